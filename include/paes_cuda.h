@@ -1,0 +1,182 @@
+/*
+ * paes_cuda.h -- C ABI of the B200-native AES-128 ECB engine (libpaes_cuda.so).
+ *
+ * Drop-in boundary for the reference "paes" library's chunked file-encryption
+ * hot path (reference tree proj/).  Every entry point is
+ * extern "C", takes plain pointers and sizes, never throws, and reports errors
+ * as negative codes that map one-to-one onto the reference's exceptions:
+ *
+ *   PAES_OK        0
+ *   PAES_EINVAL   -22   std::invalid_argument   (aes.cpp:243-245, exec.cpp:377-379, chunk.cpp:89)
+ *   PAES_EBADMSG  -74   paes::PaddingError      (chunk.cpp:120-122, 151-161)
+ *   PAES_EIO       -5   paes::IoError           (exec.cpp:48-76)
+ *   PAES_EWORKER -1001  paes::WorkerError       (exec.cpp:177-184, 300-314)
+ *   PAES_ECUDA   -1002  paes::Error (CUDA runtime failure; text in paes_cuda_last_error())
+ *   PAES_ENODEV  -1003  paes::Error (no CUDA device / bad device index)
+ *
+ * Direction: PAES_ENCRYPT = 0, PAES_DECRYPT = 1 (paes::Direction, exec.hpp:19).
+ *
+ * Round keys cross the boundary EXPANDED, as the reference's RoundKeySchedule
+ * stores them (aes.hpp:39-48, aes.cpp:151-180): 176 bytes, round key r at
+ * rk[16r .. 16r+15] in FIPS-197 byte order.  Key expansion stays on the host
+ * (paes_cuda_expand_key).  The decrypt kernels' equivalent-inverse-cipher
+ * keys are derived inside the library.
+ *
+ * Threading: all entry points are safe to call concurrently from several host
+ * threads (the reference calls encrypt_ecb from W threads at once,
+ * exec.cpp:153-175).  Host-pointer calls serialise per device on an internal
+ * lock; device-pointer calls are asynchronous on the caller's stream unless
+ * stated otherwise.
+ */
+#ifndef PAES_CUDA_H_
+#define PAES_CUDA_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PAES_OK 0
+#define PAES_EINVAL (-22)
+#define PAES_EBADMSG (-74)
+#define PAES_EIO (-5)
+#define PAES_EWORKER (-1001)
+#define PAES_ECUDA (-1002)
+#define PAES_ENODEV (-1003)
+
+#define PAES_ENCRYPT 0
+#define PAES_DECRYPT 1
+
+/* ChunkSpec (chunk.hpp:20-27), padded to a fixed 32-byte C layout. */
+typedef struct paes_chunk_spec {
+  uint64_t offset;
+  uint64_t raw_len;
+  uint64_t padded_len;
+  int32_t is_final;
+  int32_t reserved;
+} paes_chunk_spec;
+
+/* ---- library / diagnostics --------------------------------------------- */
+
+/* Text of the last error raised on the calling thread ("" if none). */
+const char* paes_cuda_last_error(void);
+/* Library version string, e.g. "paes_cuda 0.1 sm_100a". */
+const char* paes_cuda_version(void);
+/* Number of visible CUDA devices (0 when none; never an error). */
+int paes_cuda_device_count(void);
+/* Devices the host-pointer entry points shard over, in shard order (default:
+ * all visible devices).  ngpus = k uses the first k of this list.  n = 0
+ * restores the default.  One process per GPU (torchrun) sets {local_rank}. */
+int paes_cuda_set_devices(const int* ids, int n);
+/* Host-pointer pipeline tuning: staging chunk (bytes, multiple of 16) and
+ * streams per device (>= 1).  0 keeps the current value.  Defaults 32 MiB, 4. */
+int paes_cuda_set_pipeline(uint64_t chunk_bytes, int streams);
+
+/* ---- host-side rules (no GPU needed) ------------------------------------ */
+
+/* RoundKeySchedule(const Key128&) / expand_key (aes.hpp:39-50, aes.cpp:151-182). */
+int paes_cuda_expand_key(const uint8_t key[16], uint8_t rk[176]);
+
+/* plan_chunks (chunk.hpp:37-41, chunk.cpp:27-55).  Writes min(cap, n) specs
+ * and returns n (the chunk count) or a negative error. */
+int64_t paes_cuda_plan_chunks(uint64_t total_len, uint32_t workers, paes_chunk_spec* out, uint64_t cap);
+/* plan_decrypt_chunks (chunk.hpp:43-47, chunk.cpp:57-81). */
+int64_t paes_cuda_plan_decrypt_chunks(uint64_t cipher_len, uint32_t workers, paes_chunk_spec* out, uint64_t cap);
+/* pad_final (chunk.hpp:49-50, chunk.cpp:83-88): out holds (len/16+1)*16 bytes;
+ * in and out may alias.  Returns the padded length. */
+int64_t paes_cuda_pad_final(const uint8_t* raw, uint64_t len, uint8_t* out);
+/* unpad_final (chunk.hpp:52-54, chunk.cpp:90-100): unpadded length or PAES_EBADMSG. */
+int64_t paes_cuda_unpad_final(const uint8_t* padded, uint64_t len);
+
+/* ---- bulk ECB: the hot path ---------------------------------------------
+ * aes::encrypt_ecb / decrypt_ecb (aes.hpp:84-89, aes.cpp:241-265).
+ * len must be a multiple of 16 (else PAES_EINVAL); in and out may alias
+ * exactly.  Host pointers: the data is streamed H2D -> kernel -> D2H over
+ * several CUDA streams per device and sharded over `ngpus` devices
+ * (0 = all visible) as contiguous block ranges (the plan_chunks rule).
+ * Synchronous. */
+int paes_cuda_ecb(int dir, const uint8_t* in, uint8_t* out, uint64_t len, const uint8_t rk[176], int ngpus);
+
+/* Same transform on device-resident buffers of `device`, enqueued on `stream`
+ * (a cudaStream_t; NULL = legacy default stream).  Asynchronous. */
+int paes_cuda_ecb_device(int dir, const void* d_in, void* d_out, uint64_t len, const uint8_t rk[176], int device,
+                         void* stream);
+
+/* ---- chunk transforms (always-pad PKCS#7 on the final chunk) -------------
+ * encrypt_chunk / decrypt_chunk (exec.hpp:61-65, exec.cpp:111-127, 375-392).
+ * Encrypt: out holds len (non-final; len%16 must be 0) or (len/16+1)*16
+ * (final) bytes; the pad block is built on the device from the last len%16
+ * input bytes, nothing else is copied.  Decrypt: len must be a multiple of
+ * 16; a final chunk is unpadded (PAES_EBADMSG on a malformed trailer, e.g. a
+ * wrong key) and *out_len is the unpadded length.  Host pointers, sharded over
+ * `ngpus` devices like paes_cuda_ecb.  Synchronous. */
+int paes_cuda_chunk(int dir, const uint8_t* in, uint64_t len, int is_final, const uint8_t rk[176], uint8_t* out,
+                    uint64_t* out_len, int ngpus);
+
+/* Device-resident chunk transform on `stream`.  Encrypt is asynchronous and
+ * *out_len is known up front.  A final decrypt synchronises `stream` to read
+ * the pad check (the reference must inspect the trailer before it can return
+ * a length, chunk.cpp:90-100). */
+int paes_cuda_chunk_device(int dir, const void* d_in, uint64_t len, int is_final, const uint8_t rk[176], void* d_out,
+                           uint64_t* out_len, int device, void* stream);
+
+/* ---- multi-key batch (config 5) -----------------------------------------
+ * n independent messages, message i = d_in[in_off[i] .. +lens[i]) under the
+ * expanded key rks[176*i ..], written to d_out[out_off[i] ..].  Encrypt with
+ * pad=1 applies always-pad per message (output (lens[i]/16+1)*16 bytes);
+ * decrypt with pad=1 validates and strips each trailer, writing the unpadded
+ * length of message i to out_lens[i] (host array) and returning PAES_EBADMSG
+ * if any trailer is malformed (out_lens[i] = UINT64_MAX for those).  The
+ * offset/length/key arrays are host memory; one fused kernel launch per call.
+ * Synchronous when pad=1 and dir=DECRYPT, otherwise asynchronous on `stream`. */
+int paes_cuda_ecb_batch(int dir, const void* d_in, void* d_out, const uint64_t* in_off, const uint64_t* out_off,
+                        const uint64_t* lens, const uint8_t* rks, uint32_t n, int pad, uint64_t* out_lens,
+                        int device, void* stream);
+
+/* ---- file path: ExecStrategy "gpu" for run_job (exec.hpp:18-45) ---------
+ * File -> file through pinned ring buffers (pread -> H2D -> kernel -> D2H ->
+ * pwrite), output written under a temporary name and renamed on success
+ * (AtomicOutput, exec.cpp:80-106).  `workers` = number of GPUs (0 = all).
+ * Failures of individual GPU shards are reported as PAES_EWORKER with the
+ * "worker failure: chunk i: ..." text of exec.cpp:177-184. */
+typedef struct paes_job_outcome {
+  uint64_t bytes_in;
+  uint64_t bytes_out;
+  double seconds;
+} paes_job_outcome;
+
+int paes_cuda_run_job(const char* input_path, const char* output_path, const uint8_t key[16], uint32_t workers, int dir,
+                      paes_job_outcome* outcome);
+
+/* ---- synthetic inputs and device-side checks (bench / tests) ----------- */
+
+/* generate_sweep_file (bench.cpp:109-125) into memory: mt19937_64 seeded with
+ * seed_seq{seed, size}, little-endian 64-bit words, first `size` bytes. */
+int paes_cuda_sweep(uint64_t seed, uint64_t size, uint8_t* out);
+/* Config-5 message lengths. */
+int paes_cuda_batch_lengths(uint64_t seed, uint32_t n, uint64_t* lens);
+/* Counter-based stream (config 4): bytes [offset, offset+size) of the stream
+ * for `seed`, generated on `device` into d_out (offset multiple of 8). */
+int paes_cuda_counter_fill_device(uint64_t seed, uint64_t offset, uint64_t size, void* d_out, int device, void* stream);
+/* Host restatement of the same stream (for regenerating windows). */
+int paes_cuda_counter_fill(uint64_t seed, uint64_t offset, uint64_t size, uint8_t* out);
+/* Position-keyed 64-bit checksum of d_buf[0..len) (len multiple of 8), where
+ * `base_word` is the stream index of the buffer's first 64-bit word; sums of
+ * shard checksums equal the checksum of the concatenation.  Synchronous. */
+int paes_cuda_checksum_device(const void* d_buf, uint64_t len, uint64_t base_word, uint64_t* out, int device,
+                              void* stream);
+int paes_cuda_checksum(const uint8_t* buf, uint64_t len, uint64_t base_word, uint64_t* out);
+/* Number of 16-byte blocks where a and b differ.  Synchronous. */
+int paes_cuda_count_mismatch_device(const void* d_a, const void* d_b, uint64_t len, uint64_t* out, int device,
+                                    void* stream);
+
+/* Number of kernels this library launched on the calling process so far
+ * (bench.py's "gpu_launches" evidence). */
+uint64_t paes_cuda_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* PAES_CUDA_H_ */

@@ -1,0 +1,453 @@
+// aes_kernels.cu -- sm_100a kernels + their host launch wrappers.
+// See aes_kernels.cuh for the design; DESIGN.md for the roofline.
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdint>
+
+#include "aes_kernels.cuh"
+#include "launch.hpp"
+
+namespace paes_b200 {
+
+// Generated tables, constant-initialised from the constexpr host build.
+__device__ const AesTables g_tab = kTables;
+
+std::atomic<unsigned long long> g_launches{0};
+
+namespace {
+
+constexpr int kThreads = 512;  // one persistent CTA per SM (smem-limited)
+
+// ---------------------------------------------------------------- staging
+// Replicate the tables 32x (one copy per bank) into the CTA's shared memory.
+// word index w:  region = w >> 14, row x = (w >> 6) & 255, table-in-region
+// t = (w >> 5) & 1, lane = w & 31.  Four consecutive words (4 lanes) share a
+// value, so the fill is one 16-byte store per 4 words.
+template <bool DEC>
+__device__ __forceinline__ void stage_tables(std::uint32_t* sm) {
+  const std::uint32_t* base = DEC ? g_tab.td0 : g_tab.te0;
+  constexpr int nvec = (DEC ? kDecSmemBytes : kEncSmemBytes) / 16;
+  for (int i = threadIdx.x; i < nvec; i += blockDim.x) {
+    const int w = i * 4;
+    const int region = w >> 14;
+    const int x = (w >> 6) & 255;
+    const int t = (w >> 5) & 1;
+    std::uint32_t v;
+    if (region < 2) {
+      v = base[x];
+      const int rot = (region * 2 + t) * 8;
+      v = (v << rot) | (rot ? (v >> (32 - rot)) : 0u);
+    } else {
+      v = t == 0 ? static_cast<std::uint32_t>(g_tab.inv_sbox[x]) * 0x01010101u : 0u;
+    }
+    reinterpret_cast<uint4*>(sm)[i] = make_uint4(v, v, v, v);
+  }
+}
+
+// ---------------------------------------------------------------- lookups
+// (byte_k(w) << 8) | lane*4  -- one PRMT; the table offset is the LDS immediate.
+#define PAES_PERM(w, k) __byte_perm((w), lane4, 0x5504 | ((k) << 4))
+#define PAES_TL(w, k, OFF) (*reinterpret_cast<const std::uint32_t*>(smb + PAES_PERM(w, k) + (OFF)))
+
+// bytes {a.b0, b.b1, c.b2, d.b3}
+__device__ __forceinline__ std::uint32_t pick4(std::uint32_t a, std::uint32_t b, std::uint32_t c, std::uint32_t d) {
+  const std::uint32_t p = __byte_perm(a, b, 0x7650);
+  const std::uint32_t q = __byte_perm(c, d, 0x7210);
+  return __byte_perm(p, q, 0x7610);
+}
+
+struct Block4 {
+  std::uint32_t x, y, z, w;
+};
+
+// One encrypt T-round on NB blocks (round key words kw[4r..4r+3]).
+template <int NB, class K>
+__device__ __forceinline__ void enc_round(Block4 (&s)[NB], const K& kw, int r, const char* smb, std::uint32_t lane4) {
+#pragma unroll
+  for (int j = 0; j < NB; ++j) {
+    const std::uint32_t s0 = s[j].x, s1 = s[j].y, s2 = s[j].z, s3 = s[j].w;
+    s[j].x = PAES_TL(s0, 0, kT0) ^ PAES_TL(s1, 1, kT1) ^ PAES_TL(s2, 2, kT2) ^ PAES_TL(s3, 3, kT3) ^ kw[4 * r + 0];
+    s[j].y = PAES_TL(s1, 0, kT0) ^ PAES_TL(s2, 1, kT1) ^ PAES_TL(s3, 2, kT2) ^ PAES_TL(s0, 3, kT3) ^ kw[4 * r + 1];
+    s[j].z = PAES_TL(s2, 0, kT0) ^ PAES_TL(s3, 1, kT1) ^ PAES_TL(s0, 2, kT2) ^ PAES_TL(s1, 3, kT3) ^ kw[4 * r + 2];
+    s[j].w = PAES_TL(s3, 0, kT0) ^ PAES_TL(s0, 1, kT1) ^ PAES_TL(s1, 2, kT2) ^ PAES_TL(s2, 3, kT3) ^ kw[4 * r + 3];
+  }
+}
+
+// Last encrypt round: S[x] sits at byte r of Te_{(r+3)%4}[x].
+template <int NB, class K>
+__device__ __forceinline__ void enc_last(Block4 (&s)[NB], const K& kw, const char* smb, std::uint32_t lane4) {
+#pragma unroll
+  for (int j = 0; j < NB; ++j) {
+    const std::uint32_t s0 = s[j].x, s1 = s[j].y, s2 = s[j].z, s3 = s[j].w;
+    s[j].x = pick4(PAES_TL(s0, 0, kT3), PAES_TL(s1, 1, kT0), PAES_TL(s2, 2, kT1), PAES_TL(s3, 3, kT2)) ^ kw[40];
+    s[j].y = pick4(PAES_TL(s1, 0, kT3), PAES_TL(s2, 1, kT0), PAES_TL(s3, 2, kT1), PAES_TL(s0, 3, kT2)) ^ kw[41];
+    s[j].z = pick4(PAES_TL(s2, 0, kT3), PAES_TL(s3, 1, kT0), PAES_TL(s0, 2, kT1), PAES_TL(s1, 3, kT2)) ^ kw[42];
+    s[j].w = pick4(PAES_TL(s3, 0, kT3), PAES_TL(s0, 1, kT0), PAES_TL(s1, 2, kT1), PAES_TL(s2, 3, kT2)) ^ kw[43];
+  }
+}
+
+// Equivalent inverse cipher round (InvShiftRows: column j row r <- column j-r).
+template <int NB, class K>
+__device__ __forceinline__ void dec_round(Block4 (&s)[NB], const K& kw, int r, const char* smb, std::uint32_t lane4) {
+#pragma unroll
+  for (int j = 0; j < NB; ++j) {
+    const std::uint32_t s0 = s[j].x, s1 = s[j].y, s2 = s[j].z, s3 = s[j].w;
+    s[j].x = PAES_TL(s0, 0, kT0) ^ PAES_TL(s3, 1, kT1) ^ PAES_TL(s2, 2, kT2) ^ PAES_TL(s1, 3, kT3) ^ kw[4 * r + 0];
+    s[j].y = PAES_TL(s1, 0, kT0) ^ PAES_TL(s0, 1, kT1) ^ PAES_TL(s3, 2, kT2) ^ PAES_TL(s2, 3, kT3) ^ kw[4 * r + 1];
+    s[j].z = PAES_TL(s2, 0, kT0) ^ PAES_TL(s1, 1, kT1) ^ PAES_TL(s0, 2, kT2) ^ PAES_TL(s3, 3, kT3) ^ kw[4 * r + 2];
+    s[j].w = PAES_TL(s3, 0, kT0) ^ PAES_TL(s2, 1, kT1) ^ PAES_TL(s1, 2, kT2) ^ PAES_TL(s0, 3, kT3) ^ kw[4 * r + 3];
+  }
+}
+
+template <int NB, class K>
+__device__ __forceinline__ void dec_last(Block4 (&s)[NB], const K& kw, const char* smb, std::uint32_t lane4) {
+#pragma unroll
+  for (int j = 0; j < NB; ++j) {
+    const std::uint32_t s0 = s[j].x, s1 = s[j].y, s2 = s[j].z, s3 = s[j].w;
+    s[j].x = pick4(PAES_TL(s0, 0, kTS), PAES_TL(s3, 1, kTS), PAES_TL(s2, 2, kTS), PAES_TL(s1, 3, kTS)) ^ kw[40];
+    s[j].y = pick4(PAES_TL(s1, 0, kTS), PAES_TL(s0, 1, kTS), PAES_TL(s3, 2, kTS), PAES_TL(s2, 3, kTS)) ^ kw[41];
+    s[j].z = pick4(PAES_TL(s2, 0, kTS), PAES_TL(s1, 1, kTS), PAES_TL(s0, 2, kTS), PAES_TL(s3, 3, kTS)) ^ kw[42];
+    s[j].w = pick4(PAES_TL(s3, 0, kTS), PAES_TL(s2, 1, kTS), PAES_TL(s1, 2, kTS), PAES_TL(s0, 3, kTS)) ^ kw[43];
+  }
+}
+
+template <bool DEC, int NB, class K>
+__device__ __forceinline__ void cipher(Block4 (&s)[NB], const K& kw, const char* smb, std::uint32_t lane4) {
+#pragma unroll
+  for (int j = 0; j < NB; ++j) {
+    s[j].x ^= kw[0];
+    s[j].y ^= kw[1];
+    s[j].z ^= kw[2];
+    s[j].w ^= kw[3];
+  }
+#pragma unroll
+  for (int r = 1; r < 10; ++r) {
+    if (DEC) dec_round<NB>(s, kw, r, smb, lane4);
+    else enc_round<NB>(s, kw, r, smb, lane4);
+  }
+  if (DEC) dec_last<NB>(s, kw, smb, lane4);
+  else enc_last<NB>(s, kw, smb, lane4);
+}
+
+// ---------------------------------------------------------------- global I/O
+template <bool ALIGNED>
+__device__ __forceinline__ Block4 load_block(const std::uint8_t* p) {
+  if (ALIGNED) {
+    const uint4 v = __ldcs(reinterpret_cast<const uint4*>(p));
+    return Block4{v.x, v.y, v.z, v.w};
+  } else {
+    std::uint32_t w[4];
+#pragma unroll
+    for (int c = 0; c < 4; ++c)
+      w[c] = static_cast<std::uint32_t>(p[4 * c]) | (static_cast<std::uint32_t>(p[4 * c + 1]) << 8) |
+             (static_cast<std::uint32_t>(p[4 * c + 2]) << 16) | (static_cast<std::uint32_t>(p[4 * c + 3]) << 24);
+    return Block4{w[0], w[1], w[2], w[3]};
+  }
+}
+
+template <bool ALIGNED>
+__device__ __forceinline__ void store_block(std::uint8_t* p, const Block4& b) {
+  if (ALIGNED) {
+    __stcs(reinterpret_cast<uint4*>(p), make_uint4(b.x, b.y, b.z, b.w));
+  } else {
+    const std::uint32_t w[4] = {b.x, b.y, b.z, b.w};
+#pragma unroll
+    for (int c = 0; c < 16; ++c) p[c] = static_cast<std::uint8_t>(w[c >> 2] >> (8 * (c & 3)));
+  }
+}
+
+// PKCS#7 always-pad block: tail bytes then k = 16 - tail_len copies of k.
+__device__ __forceinline__ Block4 pad_block(const std::uint8_t* tail, std::uint32_t tail_len) {
+  std::uint32_t w[4];
+  const std::uint32_t k = 16u - tail_len;
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    std::uint32_t v = 0;
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const std::uint32_t i = 4 * c + b;
+      const std::uint32_t byte = i < tail_len ? tail[i] : k;
+      v |= byte << (8 * b);
+    }
+    w[c] = v;
+  }
+  return Block4{w[0], w[1], w[2], w[3]};
+}
+
+// PKCS#7 trailer check of a decrypted last block (chunk.cpp:151-161).
+__device__ __forceinline__ std::uint32_t pad_check(const Block4& b) {
+  const std::uint32_t w[4] = {b.x, b.y, b.z, b.w};
+  const std::uint32_t k = b.w >> 24;
+  bool ok = k >= 1 && k <= 16;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    const std::uint32_t byte = (w[i >> 2] >> (8 * (i & 3))) & 0xff;
+    if (i >= 16 - static_cast<int>(k) && byte != k) ok = false;
+  }
+  return ok ? k : 0xffffffffu;
+}
+
+// ---------------------------------------------------------------- single key
+template <bool DEC, int NB, bool ALIGNED>
+__global__ void __launch_bounds__(kThreads, 1) ecb_kernel(const __grid_constant__ EcbArgs a) {
+  extern __shared__ __align__(16) std::uint32_t sm[];
+  stage_tables<DEC>(sm);
+  __syncthreads();
+  const char* smb = reinterpret_cast<const char*>(sm);
+  const std::uint32_t lane = threadIdx.x & 31;
+  const std::uint32_t lane4 = lane * 4;
+  constexpr unsigned long long kTile = 32ull * NB;
+  const unsigned long long ntiles = (a.nblocks + kTile - 1) / kTile;
+  // tiles of whole input blocks; the tile holding a checked trailer goes to
+  // the ragged loop so the pad check always runs
+  const unsigned long long full_tiles = (a.check_pad ? a.nfull - 1 : a.nfull) / kTile;
+  const unsigned long long wpc = blockDim.x / 32;
+  unsigned long long tile = blockIdx.x * wpc + threadIdx.x / 32;
+  const unsigned long long tstride = gridDim.x * wpc;
+
+  // steady state: whole tiles of whole input blocks, no per-block checks
+  for (; tile < full_tiles; tile += tstride) {
+    const unsigned long long b0 = tile * kTile + lane;
+    Block4 s[NB];
+#pragma unroll
+    for (int j = 0; j < NB; ++j) s[j] = load_block<ALIGNED>(a.in + 16ull * (b0 + 32ull * j));
+    cipher<DEC, NB>(s, a.k.w, smb, lane4);
+#pragma unroll
+    for (int j = 0; j < NB; ++j) store_block<ALIGNED>(a.out + 16ull * (b0 + 32ull * j), s[j]);
+  }
+  // the (at most one) ragged tile: partial blocks, pad block, trailer check
+  for (; tile < ntiles; tile += tstride) {
+    const unsigned long long b0 = tile * kTile + lane;
+    Block4 s[NB];
+#pragma unroll
+    for (int j = 0; j < NB; ++j) {
+      const unsigned long long idx = b0 + 32ull * j;
+      if (idx < a.nfull) s[j] = load_block<ALIGNED>(a.in + 16ull * idx);
+      else if (idx < a.nblocks) s[j] = pad_block(a.in + 16ull * a.nfull, a.tail_len);
+      else s[j] = Block4{0, 0, 0, 0};
+    }
+    cipher<DEC, NB>(s, a.k.w, smb, lane4);
+#pragma unroll
+    for (int j = 0; j < NB; ++j) {
+      const unsigned long long idx = b0 + 32ull * j;
+      if (idx < a.nblocks) {
+        store_block<ALIGNED>(a.out + 16ull * idx, s[j]);
+        if (DEC && a.check_pad && idx == a.nblocks - 1) *a.status = pad_check(s[j]);
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------- batch
+// Persistent warps over a contiguous range of warp tiles of the concatenated
+// block stream; a warp's tiles advance monotonically through the messages,
+// so its key registers are reloaded only when it crosses a message.
+template <bool DEC, int NB>
+__global__ void __launch_bounds__(kThreads, 1) batch_kernel(const __grid_constant__ BatchArgs a) {
+  extern __shared__ __align__(16) std::uint32_t sm[];
+  stage_tables<DEC>(sm);
+  __syncthreads();
+  const char* smb = reinterpret_cast<const char*>(sm);
+  const std::uint32_t lane = threadIdx.x & 31;
+  const std::uint32_t lane4 = lane * 4;
+  constexpr unsigned long long kTile = 32ull * NB;
+  const unsigned long long ntiles = (a.total_blocks + kTile - 1) / kTile;
+  const unsigned long long nwarps = static_cast<unsigned long long>(gridDim.x) * (blockDim.x / 32);
+  const unsigned long long warp = static_cast<unsigned long long>(blockIdx.x) * (blockDim.x / 32) + threadIdx.x / 32;
+  const unsigned long long t_begin = ntiles * warp / nwarps;
+  const unsigned long long t_end = ntiles * (warp + 1) / nwarps;
+  if (t_begin >= t_end) return;
+
+  // message holding the warp's first block (binary search, warp-uniform)
+  std::uint32_t m = 0;
+  {
+    const unsigned long long g0 = t_begin * kTile;
+    std::uint32_t lo = 0, hi = a.nmsg;  // last msg with first <= g0
+    while (hi - lo > 1) {
+      const std::uint32_t mid = (lo + hi) / 2;
+      if (a.msgs[mid].first <= g0) lo = mid;
+      else hi = mid;
+    }
+    m = lo;
+  }
+  std::uint32_t kw[44];
+  std::uint32_t key_m = 0xffffffffu;
+  for (unsigned long long tile = t_begin; tile < t_end; ++tile) {
+    const unsigned long long g0 = tile * kTile;
+    const unsigned long long g_last = min(g0 + kTile, a.total_blocks) - 1;
+    while (m + 1 < a.nmsg && a.msgs[m + 1].first <= g0) ++m;
+    const BatchMsg msg = a.msgs[m];
+    if (g0 + kTile <= a.total_blocks && g_last + a.check_pad < msg.first + msg.nfull) {
+      // fast path: the whole tile is whole input blocks of message m
+      if (key_m != m) {
+        const uint4* kp = reinterpret_cast<const uint4*>(a.keys + 44ull * m);
+#pragma unroll
+        for (int i = 0; i < 11; ++i) {
+          const uint4 v = __ldg(kp + i);
+          kw[4 * i] = v.x;
+          kw[4 * i + 1] = v.y;
+          kw[4 * i + 2] = v.z;
+          kw[4 * i + 3] = v.w;
+        }
+        key_m = m;
+      }
+      const unsigned long long lb = g0 - msg.first + lane;
+      const std::uint8_t* src = a.in + msg.in_off + 16ull * lb;
+      std::uint8_t* dst = a.out + msg.out_off + 16ull * lb;
+      Block4 s[NB];
+#pragma unroll
+      for (int j = 0; j < NB; ++j) s[j] = load_block<true>(src + 512ull * j);
+      cipher<DEC, NB>(s, kw, smb, lane4);
+#pragma unroll
+      for (int j = 0; j < NB; ++j) store_block<true>(dst + 512ull * j, s[j]);
+    } else {
+      // boundary tile: block by block, keys read from global per message
+#pragma unroll 1
+      for (int j = 0; j < NB; ++j) {
+        const unsigned long long g = g0 + lane + 32ull * j;
+        if (g >= a.total_blocks) break;
+        std::uint32_t mm = m;
+        while (mm + 1 < a.nmsg && a.msgs[mm + 1].first <= g) ++mm;
+        const BatchMsg bm = a.msgs[mm];
+        const unsigned long long lb = g - bm.first;
+        Block4 s1[1];
+        if (lb < bm.nfull) s1[0] = load_block<true>(a.in + bm.in_off + 16ull * lb);
+        else s1[0] = pad_block(a.in + bm.in_off + 16ull * bm.nfull, bm.tail_len);
+        const std::uint32_t* gk = a.keys + 44ull * mm;
+        cipher<DEC, 1>(s1, gk, smb, lane4);
+        store_block<true>(a.out + bm.out_off + 16ull * lb, s1[0]);
+        if (DEC && a.check_pad && lb == bm.nblocks - 1) a.status[mm] = pad_check(s1[0]);
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------- utilities
+__device__ __forceinline__ unsigned long long mix64(unsigned long long z) {
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+// word i of the config-4 stream (oracle_counter_fill restates it on the CPU)
+__device__ __forceinline__ unsigned long long counter_word(unsigned long long seed, unsigned long long i) {
+  return mix64(seed * 0xD1B54A32D192ED03ull + (i + 1) * 0x9E3779B97F4A7C15ull);
+}
+
+__global__ void counter_fill_kernel(unsigned long long seed, unsigned long long word0, unsigned long long nwords,
+                                    unsigned long long* out) {
+  const unsigned long long stride = static_cast<unsigned long long>(gridDim.x) * blockDim.x;
+  const unsigned long long npairs = nwords / 2;
+  for (unsigned long long p = static_cast<unsigned long long>(blockIdx.x) * blockDim.x + threadIdx.x; p < npairs;
+       p += stride) {
+    const unsigned long long i = word0 + 2 * p;
+    reinterpret_cast<ulonglong2*>(out)[p] = make_ulonglong2(counter_word(seed, i), counter_word(seed, i + 1));
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0 && (nwords & 1)) out[nwords - 1] = counter_word(seed, word0 + nwords - 1);
+}
+
+__global__ void checksum_kernel(const unsigned long long* buf, unsigned long long nwords, unsigned long long base,
+                                unsigned long long* out) {
+  const unsigned long long stride = static_cast<unsigned long long>(gridDim.x) * blockDim.x;
+  unsigned long long acc = 0;
+  for (unsigned long long i = static_cast<unsigned long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < nwords;
+       i += stride)
+    acc += mix64(buf[i] ^ ((base + i) * 0x9E3779B97F4A7C15ull));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31) == 0) atomicAdd(out, acc);
+}
+
+__global__ void mismatch_kernel(const uint4* a, const uint4* b, unsigned long long nblocks, unsigned long long* out) {
+  const unsigned long long stride = static_cast<unsigned long long>(gridDim.x) * blockDim.x;
+  unsigned int cnt = 0;
+  for (unsigned long long i = static_cast<unsigned long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < nblocks;
+       i += stride) {
+    const uint4 x = a[i], y = b[i];
+    cnt += (x.x != y.x) | (x.y != y.y) | (x.z != y.z) | (x.w != y.w);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+  if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(out, static_cast<unsigned long long>(cnt));
+}
+
+template <class KernelT>
+cudaError_t set_smem(KernelT k, int bytes) {
+  return cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------- launchers
+constexpr int kNB = 2;  // blocks per thread per warp tile
+
+cudaError_t prepare_kernels() {
+  cudaError_t e;
+  if ((e = set_smem(ecb_kernel<false, kNB, true>, kEncSmemBytes))) return e;
+  if ((e = set_smem(ecb_kernel<false, kNB, false>, kEncSmemBytes))) return e;
+  if ((e = set_smem(ecb_kernel<true, kNB, true>, kDecSmemBytes))) return e;
+  if ((e = set_smem(ecb_kernel<true, kNB, false>, kDecSmemBytes))) return e;
+  if ((e = set_smem(batch_kernel<false, kNB>, kEncSmemBytes))) return e;
+  if ((e = set_smem(batch_kernel<true, kNB>, kDecSmemBytes))) return e;
+  return cudaSuccess;
+}
+
+cudaError_t launch_ecb(bool dec, const EcbArgs& args, int sm_count, cudaStream_t stream) {
+  if (args.nblocks == 0) return cudaSuccess;
+  const unsigned long long per_cta = static_cast<unsigned long long>(kThreads) * kNB;
+  unsigned long long grid = (args.nblocks + per_cta - 1) / per_cta;
+  if (grid > static_cast<unsigned long long>(sm_count)) grid = sm_count;
+  const bool aligned = ((reinterpret_cast<std::uintptr_t>(args.in) | reinterpret_cast<std::uintptr_t>(args.out)) & 15) == 0;
+  const int smem = dec ? kDecSmemBytes : kEncSmemBytes;
+  if (dec) {
+    if (aligned) ecb_kernel<true, kNB, true><<<static_cast<unsigned>(grid), kThreads, smem, stream>>>(args);
+    else ecb_kernel<true, kNB, false><<<static_cast<unsigned>(grid), kThreads, smem, stream>>>(args);
+  } else {
+    if (aligned) ecb_kernel<false, kNB, true><<<static_cast<unsigned>(grid), kThreads, smem, stream>>>(args);
+    else ecb_kernel<false, kNB, false><<<static_cast<unsigned>(grid), kThreads, smem, stream>>>(args);
+  }
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_batch(bool dec, const BatchArgs& args, int sm_count, cudaStream_t stream) {
+  if (args.total_blocks == 0) return cudaSuccess;
+  const unsigned long long per_cta = static_cast<unsigned long long>(kThreads) * kNB;
+  unsigned long long grid = (args.total_blocks + per_cta - 1) / per_cta;
+  if (grid > static_cast<unsigned long long>(sm_count)) grid = sm_count;
+  const int smem = dec ? kDecSmemBytes : kEncSmemBytes;
+  if (dec) batch_kernel<true, kNB><<<static_cast<unsigned>(grid), kThreads, smem, stream>>>(args);
+  else batch_kernel<false, kNB><<<static_cast<unsigned>(grid), kThreads, smem, stream>>>(args);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_counter_fill(unsigned long long seed, unsigned long long word0, unsigned long long nwords, void* out,
+                                int sm_count, cudaStream_t stream) {
+  if (nwords == 0) return cudaSuccess;
+  counter_fill_kernel<<<sm_count * 4, 512, 0, stream>>>(seed, word0, nwords, static_cast<unsigned long long*>(out));
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_checksum(const void* buf, unsigned long long nwords, unsigned long long base, unsigned long long* d_out,
+                            int sm_count, cudaStream_t stream) {
+  if (nwords == 0) return cudaSuccess;
+  checksum_kernel<<<sm_count * 4, 512, 0, stream>>>(static_cast<const unsigned long long*>(buf), nwords, base, d_out);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_mismatch(const void* a, const void* b, unsigned long long nblocks, unsigned long long* d_out,
+                            int sm_count, cudaStream_t stream) {
+  if (nblocks == 0) return cudaSuccess;
+  mismatch_kernel<<<sm_count * 4, 512, 0, stream>>>(static_cast<const uint4*>(a), static_cast<const uint4*>(b), nblocks,
+                                                   d_out);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return cudaGetLastError();
+}
+
+unsigned long long launch_count() { return g_launches.load(std::memory_order_relaxed); }
+
+}  // namespace paes_b200

@@ -1,0 +1,797 @@
+// paes_cuda.cu -- the C ABI (include/paes_cuda.h) and the host runtime around
+// the sm_100a kernels: per-device contexts, the multi-stream host<->device
+// pipeline, the multi-GPU block-range sharder and the file pipeline.
+//
+// Reference boundary: aes::encrypt_ecb/decrypt_ecb
+// (aes.hpp:86-89), paes::encrypt_chunk/decrypt_chunk (exec.hpp:61-65) and
+// run_job's strategy dispatch (exec.cpp:340-347).  Exceptions become codes:
+// std::invalid_argument -> PAES_EINVAL, PaddingError -> PAES_EBADMSG,
+// IoError -> PAES_EIO, WorkerError -> PAES_EWORKER, CUDA -> PAES_ECUDA.
+#include <cuda_runtime.h>
+#include <fcntl.h>
+#include <sys/stat.h>
+#include <unistd.h>
+
+#include <algorithm>
+#include <cerrno>
+#include <chrono>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <sstream>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "../../include/paes_cuda.h"
+#include "host_rules.hpp"
+#include "launch.hpp"
+
+using namespace paes_b200;
+
+namespace {
+
+thread_local std::string t_err;
+
+int fail(int code, const std::string& msg) {
+  t_err = msg;
+  return code;
+}
+
+struct CudaFail {
+  int code;
+  std::string msg;
+};
+
+#define PAES_CK(call)                                                                           \
+  do {                                                                                          \
+    const cudaError_t e_ = (call);                                                              \
+    if (e_ != cudaSuccess) throw CudaFail{PAES_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e_)}; \
+  } while (0)
+
+// Runs `f`, mapping C++ exceptions to C-ABI codes (no exception crosses the ABI).
+template <class F>
+int guarded(F&& f) {
+  try {
+    return f();
+  } catch (const CudaFail& e) {
+    return fail(e.code, e.msg);
+  } catch (const PaddingError& e) {
+    return fail(PAES_EBADMSG, e.what());
+  } catch (const std::invalid_argument& e) {
+    return fail(PAES_EINVAL, e.what());
+  } catch (const std::bad_alloc&) {
+    return fail(PAES_ECUDA, "host allocation failed");
+  } catch (const std::exception& e) {
+    return fail(PAES_ECUDA, e.what());
+  }
+}
+
+class DeviceGuard {
+ public:
+  explicit DeviceGuard(int dev) {
+    if (cudaGetDevice(&prev_) != cudaSuccess) prev_ = -1;
+    if (prev_ != dev) PAES_CK(cudaSetDevice(dev));
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    if (prev_ >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev_) cudaSetDevice(prev_);
+  }
+
+ private:
+  int prev_ = -1;
+};
+
+// ------------------------------------------------------------ device context
+struct DevCtx {
+  int id = -1;
+  bool ready = false;
+  int sm_count = 0;
+  std::mutex mu;  // serialises host-pointer pipelines / status words on this device
+  std::vector<cudaStream_t> st;
+  std::vector<std::uint8_t*> dbuf;  // chunk + 16 bytes each
+  std::vector<std::uint8_t*> hbuf;  // pinned staging for the file path
+  std::vector<cudaEvent_t> ev;
+  std::uint64_t chunk = 0;
+  std::uint32_t* d_status = nullptr;
+  std::uint32_t* h_status = nullptr;  // pinned
+  unsigned long long* d_acc = nullptr;
+  unsigned long long* h_acc = nullptr;  // pinned
+};
+
+constexpr int kMaxDev = 64;
+DevCtx g_dev[kMaxDev];
+std::mutex g_cfg_mu;
+std::vector<int> g_devices;  // empty = all visible
+std::uint64_t g_chunk = 32ull << 20;
+int g_streams = 4;
+
+int visible_devices() {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
+
+// Lazily initialise a device: kernel attributes, status words.
+DevCtx& device(int id) {
+  const int n = visible_devices();
+  if (id < 0 || id >= n || id >= kMaxDev)
+    throw CudaFail{PAES_ENODEV, "no such CUDA device: " + std::to_string(id) + " (visible: " + std::to_string(n) + ")"};
+  DevCtx& d = g_dev[id];
+  std::lock_guard<std::mutex> lk(d.mu);
+  if (!d.ready) {
+    DeviceGuard g(id);
+    PAES_CK(cudaDeviceGetAttribute(&d.sm_count, cudaDevAttrMultiProcessorCount, id));
+    PAES_CK(prepare_kernels());
+    PAES_CK(cudaMalloc(&d.d_status, 4096));
+    PAES_CK(cudaMallocHost(&d.h_status, 4096));
+    PAES_CK(cudaMalloc(&d.d_acc, 64));
+    PAES_CK(cudaMallocHost(&d.h_acc, 64));
+    d.id = id;
+    d.ready = true;
+  }
+  return d;
+}
+
+// Pipeline buffers (device rings + optional pinned host ring); d.mu held.
+void ensure_pipeline(DevCtx& d, bool need_host) {
+  std::uint64_t chunk;
+  int ns;
+  {
+    std::lock_guard<std::mutex> lk(g_cfg_mu);
+    chunk = g_chunk;
+    ns = g_streams;
+  }
+  if (d.chunk != chunk || static_cast<int>(d.st.size()) != ns) {
+    for (auto p : d.dbuf) cudaFree(p);
+    for (auto p : d.hbuf) cudaFreeHost(p);
+    for (auto s : d.st) cudaStreamDestroy(s);
+    for (auto e : d.ev) cudaEventDestroy(e);
+    d.dbuf.clear();
+    d.hbuf.clear();
+    d.st.clear();
+    d.ev.clear();
+    d.chunk = chunk;
+    for (int i = 0; i < ns; ++i) {
+      cudaStream_t s;
+      PAES_CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+      d.st.push_back(s);
+      cudaEvent_t e;
+      PAES_CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      d.ev.push_back(e);
+      std::uint8_t* p = nullptr;
+      PAES_CK(cudaMalloc(&p, chunk + 16));
+      d.dbuf.push_back(p);
+    }
+  }
+  if (need_host && d.hbuf.empty()) {
+    for (int i = 0; i < ns; ++i) {
+      std::uint8_t* p = nullptr;
+      PAES_CK(cudaMallocHost(&p, d.chunk + 16));
+      d.hbuf.push_back(p);
+    }
+  }
+}
+
+std::vector<int> device_list(int ngpus) {
+  std::vector<int> list;
+  {
+    std::lock_guard<std::mutex> lk(g_cfg_mu);
+    list = g_devices;
+  }
+  if (list.empty()) {
+    const int n = visible_devices();
+    for (int i = 0; i < n; ++i) list.push_back(i);
+  }
+  if (list.empty()) throw CudaFail{PAES_ENODEV, "no CUDA device visible"};
+  if (ngpus < 0) throw std::invalid_argument("ngpus must be >= 0");
+  if (ngpus > 0) {
+    if (ngpus > static_cast<int>(list.size()))
+      throw CudaFail{PAES_ENODEV, "requested " + std::to_string(ngpus) + " GPUs, " + std::to_string(list.size()) +
+                                      " available"};
+    list.resize(ngpus);
+  }
+  return list;
+}
+
+// ------------------------------------------------------------ pieces
+// A transform over one contiguous range: whole input blocks, plus (encrypt,
+// final) the always-pad block built from `tail` trailing bytes, plus
+// (decrypt, final) a trailer check on the last block.
+struct Range {
+  bool dec = false;
+  bool pad = false;        // encrypt: append the PKCS#7 block
+  bool check_pad = false;  // decrypt: validate the trailer
+  std::uint64_t in_len = 0;
+};
+
+EcbArgs make_args(const Range& r, const std::uint8_t* in, std::uint8_t* out, std::uint64_t in_len, bool last,
+                  const KeyWords& kw, std::uint32_t* status) {
+  EcbArgs a{};
+  a.in = in;
+  a.out = out;
+  a.nfull = in_len / 16;
+  a.tail_len = static_cast<std::uint32_t>(in_len % 16);
+  a.nblocks = a.nfull + ((r.pad && last) ? 1 : 0);
+  a.check_pad = (r.check_pad && last) ? 1u : 0u;
+  a.status = status;
+  a.k = kw;
+  return a;
+}
+
+// Host range on one device through the stream ring (d.mu held).  Returns the
+// number of output bytes (decrypt+check: unpadded).
+std::uint64_t run_host_range(DevCtx& d, const Range& r, const std::uint8_t* in, std::uint8_t* out, const KeyWords& kw) {
+  DeviceGuard g(d.id);
+  ensure_pipeline(d, false);
+  const std::uint64_t C = d.chunk;
+  const int S = static_cast<int>(d.st.size());
+  const std::uint64_t npieces = std::max<std::uint64_t>(1, (r.in_len + C - 1) / C);
+  std::uint64_t out_total = 0;
+  for (std::uint64_t k = 0; k < npieces; ++k) {
+    const int s = static_cast<int>(k % S);
+    const std::uint64_t off = k * C;
+    const std::uint64_t len = std::min<std::uint64_t>(C, r.in_len - off);
+    const bool last = k + 1 == npieces;
+    EcbArgs a = make_args(r, d.dbuf[s], d.dbuf[s], len, last, kw, d.d_status);
+    if (len) PAES_CK(cudaMemcpyAsync(d.dbuf[s], in + off, len, cudaMemcpyHostToDevice, d.st[s]));
+    if (a.check_pad) PAES_CK(cudaMemsetAsync(d.d_status, 0xff, 4, d.st[s]));  // sentinel: unchecked => PaddingError
+    PAES_CK(launch_ecb(r.dec, a, d.sm_count, d.st[s]));
+    const std::uint64_t olen = a.nblocks * 16;
+    if (olen) PAES_CK(cudaMemcpyAsync(out + off, d.dbuf[s], olen, cudaMemcpyDeviceToHost, d.st[s]));
+    if (last && a.check_pad)
+      PAES_CK(cudaMemcpyAsync(d.h_status, d.d_status, 4, cudaMemcpyDeviceToHost, d.st[s]));
+    out_total = off + olen;
+  }
+  for (auto s : d.st) PAES_CK(cudaStreamSynchronize(s));
+  if (r.check_pad) {
+    const std::uint32_t k = *d.h_status;
+    if (k == 0xffffffffu) throw PaddingError("unpad: invalid pad bytes");
+    out_total -= k;
+  }
+  return out_total;
+}
+
+// Shard a host buffer over devices with the plan_chunks rule (encrypt) or
+// plan_decrypt_chunks (decrypt); output offsets equal input offsets.
+int host_transform(int dir, const std::uint8_t* in, std::uint64_t len, bool is_final, const std::uint8_t* rk,
+                   std::uint8_t* out, std::uint64_t* out_len, int ngpus) {
+  if (dir != PAES_ENCRYPT && dir != PAES_DECRYPT) throw std::invalid_argument("dir must be 0 (encrypt) or 1 (decrypt)");
+  if (!rk) throw std::invalid_argument("null round keys");
+  const bool dec = dir == PAES_DECRYPT;
+  if (!is_final && len % 16 != 0) throw std::invalid_argument("non-final chunk length must be a multiple of 16");
+  if (dec && len % 16 != 0) throw std::invalid_argument("decrypt: length must be a multiple of 16");
+  if (len && !in) throw std::invalid_argument("null input");
+  if (dec && is_final && len == 0) throw PaddingError("unpad: length must be a non-zero multiple of 16");
+  if (len == 0 && !(is_final && !dec)) {
+    if (out_len) *out_len = 0;
+    return PAES_OK;
+  }
+  if (!out) throw std::invalid_argument("null output");
+  const auto devs = device_list(ngpus);
+  const KeyWords kw = dec ? dec_key_words(rk) : enc_key_words(rk);
+  const auto plan = dec ? plan_decrypt_chunks(len, static_cast<unsigned>(devs.size()))
+                        : plan_chunks(len, static_cast<unsigned>(devs.size()));
+  std::vector<std::uint64_t> produced(plan.size(), 0);
+  std::vector<int> codes(plan.size(), PAES_OK);
+  std::vector<std::string> msgs(plan.size());
+  auto work = [&](std::size_t i) {
+    const Chunk& c = plan[i];
+    Range r;
+    r.dec = dec;
+    r.in_len = c.raw_len;
+    r.pad = !dec && is_final && c.is_final;
+    r.check_pad = dec && is_final && c.is_final;
+    codes[i] = guarded([&] {
+      DevCtx& d = device(devs[i]);
+      std::lock_guard<std::mutex> lk(d.mu);
+      produced[i] = run_host_range(d, r, in + c.offset, out + c.offset, kw);
+      return PAES_OK;
+    });
+    if (codes[i]) msgs[i] = t_err;
+  };
+  if (plan.size() == 1) {
+    work(0);
+  } else {
+    std::vector<std::thread> pool;
+    for (std::size_t i = 0; i < plan.size(); ++i) pool.emplace_back(work, i);
+    for (auto& t : pool) t.join();
+  }
+  for (std::size_t i = 0; i < plan.size(); ++i)
+    if (codes[i]) return fail(codes[i], msgs[i]);
+  std::uint64_t total = 0;
+  for (auto p : produced) total += p;
+  if (out_len) *out_len = total;
+  return PAES_OK;
+}
+
+}  // namespace
+
+// ============================================================ C ABI
+extern "C" {
+
+const char* paes_cuda_last_error(void) { return t_err.c_str(); }
+
+const char* paes_cuda_version(void) { return "paes_cuda 0.1 sm_100a (T-table smem x32, PRMT-addressed)"; }
+
+int paes_cuda_device_count(void) { return visible_devices(); }
+
+int paes_cuda_set_devices(const int* ids, int n) {
+  return guarded([&] {
+    if (n < 0 || (n > 0 && !ids)) throw std::invalid_argument("bad device list");
+    const int vis = visible_devices();
+    for (int i = 0; i < n; ++i)
+      if (ids[i] < 0 || ids[i] >= vis) throw CudaFail{PAES_ENODEV, "no such CUDA device: " + std::to_string(ids[i])};
+    std::lock_guard<std::mutex> lk(g_cfg_mu);
+    g_devices.assign(ids, ids + n);
+    return PAES_OK;
+  });
+}
+
+int paes_cuda_set_pipeline(uint64_t chunk_bytes, int streams) {
+  return guarded([&] {
+    if (chunk_bytes % 16 != 0) throw std::invalid_argument("chunk_bytes must be a multiple of 16");
+    if (streams < 0) throw std::invalid_argument("streams must be >= 0");
+    std::lock_guard<std::mutex> lk(g_cfg_mu);
+    if (chunk_bytes) g_chunk = chunk_bytes;
+    if (streams) g_streams = streams;
+    return PAES_OK;
+  });
+}
+
+int paes_cuda_expand_key(const uint8_t key[16], uint8_t rk[176]) {
+  return guarded([&] {
+    if (!key || !rk) throw std::invalid_argument("null key");
+    expand_key(key, rk);
+    return PAES_OK;
+  });
+}
+
+static int64_t plan_out(const std::vector<Chunk>& p, paes_chunk_spec* out, uint64_t cap) {
+  for (std::size_t i = 0; i < p.size() && i < cap; ++i)
+    out[i] = paes_chunk_spec{p[i].offset, p[i].raw_len, p[i].padded_len, p[i].is_final ? 1 : 0, 0};
+  return static_cast<int64_t>(p.size());
+}
+
+int64_t paes_cuda_plan_chunks(uint64_t total_len, uint32_t workers, paes_chunk_spec* out, uint64_t cap) {
+  int64_t n = 0;
+  const int rc = guarded([&] {
+    n = plan_out(plan_chunks(total_len, workers), out, out ? cap : 0);
+    return PAES_OK;
+  });
+  return rc ? rc : n;
+}
+
+int64_t paes_cuda_plan_decrypt_chunks(uint64_t cipher_len, uint32_t workers, paes_chunk_spec* out, uint64_t cap) {
+  int64_t n = 0;
+  const int rc = guarded([&] {
+    n = plan_out(plan_decrypt_chunks(cipher_len, workers), out, out ? cap : 0);
+    return PAES_OK;
+  });
+  return rc ? rc : n;
+}
+
+int64_t paes_cuda_pad_final(const uint8_t* raw, uint64_t len, uint8_t* out) {
+  if ((len && !raw) || !out) return fail(PAES_EINVAL, "null buffer");
+  const uint64_t k = 16 - len % 16;
+  if (len && raw != out) std::memmove(out, raw, len);
+  std::memset(out + len, static_cast<int>(k), k);
+  return static_cast<int64_t>(len + k);
+}
+
+int64_t paes_cuda_unpad_final(const uint8_t* padded, uint64_t len) {
+  int64_t n = 0;
+  const int rc = guarded([&] {
+    if (len && !padded) throw std::invalid_argument("null buffer");
+    n = static_cast<int64_t>(unpad_final(padded, len));
+    return PAES_OK;
+  });
+  return rc ? rc : n;
+}
+
+int paes_cuda_ecb(int dir, const uint8_t* in, uint8_t* out, uint64_t len, const uint8_t rk[176], int ngpus) {
+  return guarded([&] {
+    if (len % 16 != 0) throw std::invalid_argument("ecb: length must be a multiple of 16 and match output");
+    return host_transform(dir, in, len, false, rk, out, nullptr, ngpus);
+  });
+}
+
+int paes_cuda_chunk(int dir, const uint8_t* in, uint64_t len, int is_final, const uint8_t rk[176], uint8_t* out,
+                    uint64_t* out_len, int ngpus) {
+  return guarded([&] { return host_transform(dir, in, len, is_final != 0, rk, out, out_len, ngpus); });
+}
+
+int paes_cuda_ecb_device(int dir, const void* d_in, void* d_out, uint64_t len, const uint8_t rk[176], int device_id,
+                         void* stream) {
+  return guarded([&] {
+    if (dir != PAES_ENCRYPT && dir != PAES_DECRYPT) throw std::invalid_argument("bad dir");
+    if (len % 16 != 0) throw std::invalid_argument("ecb: length must be a multiple of 16 and match output");
+    if (!rk) throw std::invalid_argument("null round keys");
+    if (len == 0) return PAES_OK;
+    if (!d_in || !d_out) throw std::invalid_argument("null device buffer");
+    DevCtx& d = device(device_id);
+    DeviceGuard g(device_id);
+    const bool dec = dir == PAES_DECRYPT;
+    Range r;
+    r.dec = dec;
+    EcbArgs a = make_args(r, static_cast<const std::uint8_t*>(d_in), static_cast<std::uint8_t*>(d_out), len, true,
+                          dec ? dec_key_words(rk) : enc_key_words(rk), nullptr);
+    PAES_CK(launch_ecb(dec, a, d.sm_count, static_cast<cudaStream_t>(stream)));
+    return PAES_OK;
+  });
+}
+
+int paes_cuda_chunk_device(int dir, const void* d_in, uint64_t len, int is_final, const uint8_t rk[176], void* d_out,
+                           uint64_t* out_len, int device_id, void* stream) {
+  return guarded([&] {
+    if (dir != PAES_ENCRYPT && dir != PAES_DECRYPT) throw std::invalid_argument("bad dir");
+    if (!rk) throw std::invalid_argument("null round keys");
+    const bool dec = dir == PAES_DECRYPT;
+    const bool final = is_final != 0;
+    if (!final && len % 16 != 0) throw std::invalid_argument("non-final chunk length must be a multiple of 16");
+    if (dec && len % 16 != 0) throw std::invalid_argument("decrypt: length must be a multiple of 16");
+    if (dec && final && len == 0) throw PaddingError("unpad: length must be a non-zero multiple of 16");
+    Range r;
+    r.dec = dec;
+    r.pad = !dec && final;
+    r.check_pad = dec && final;
+    if (len == 0 && !r.pad) {
+      if (out_len) *out_len = 0;
+      return PAES_OK;
+    }
+    if ((len && !d_in) || !d_out) throw std::invalid_argument("null device buffer");
+    DevCtx& d = device(device_id);
+    DeviceGuard g(device_id);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (!r.check_pad) {
+      EcbArgs a = make_args(r, static_cast<const std::uint8_t*>(d_in), static_cast<std::uint8_t*>(d_out), len, true,
+                            dec ? dec_key_words(rk) : enc_key_words(rk), nullptr);
+      PAES_CK(launch_ecb(dec, a, d.sm_count, s));
+      if (out_len) *out_len = a.nblocks * 16;
+      return PAES_OK;
+    }
+    std::lock_guard<std::mutex> lk(d.mu);
+    EcbArgs a = make_args(r, static_cast<const std::uint8_t*>(d_in), static_cast<std::uint8_t*>(d_out), len, true,
+                          dec_key_words(rk), d.d_status);
+    PAES_CK(cudaMemsetAsync(d.d_status, 0xff, 4, s));
+    PAES_CK(launch_ecb(true, a, d.sm_count, s));
+    PAES_CK(cudaMemcpyAsync(d.h_status, d.d_status, 4, cudaMemcpyDeviceToHost, s));
+    PAES_CK(cudaStreamSynchronize(s));
+    const std::uint32_t k = *d.h_status;
+    if (k == 0xffffffffu) throw PaddingError("unpad: invalid pad bytes");
+    if (out_len) *out_len = len - k;
+    return PAES_OK;
+  });
+}
+
+int paes_cuda_ecb_batch(int dir, const void* d_in, void* d_out, const uint64_t* in_off, const uint64_t* out_off,
+                        const uint64_t* lens, const uint8_t* rks, uint32_t n, int pad, uint64_t* out_lens,
+                        int device_id, void* stream) {
+  return guarded([&] {
+    if (dir != PAES_ENCRYPT && dir != PAES_DECRYPT) throw std::invalid_argument("bad dir");
+    if (n == 0) return PAES_OK;
+    if (!in_off || !out_off || !lens || !rks) throw std::invalid_argument("null batch descriptor");
+    const bool dec = dir == PAES_DECRYPT;
+    std::vector<BatchMsg> msgs(n);
+    std::vector<KeyWords> keys(n);
+    unsigned long long g = 0;
+    for (uint32_t i = 0; i < n; ++i) {
+      if (in_off[i] % 16 || out_off[i] % 16) throw std::invalid_argument("batch offsets must be multiples of 16");
+      if ((dec || !pad) && lens[i] % 16) throw std::invalid_argument("message length must be a multiple of 16");
+      if (dec && pad && lens[i] == 0) throw PaddingError("unpad: length must be a non-zero multiple of 16");
+      BatchMsg& m = msgs[i];
+      m.in_off = in_off[i];
+      m.out_off = out_off[i];
+      m.first = g;
+      m.nfull = lens[i] / 16;
+      m.tail_len = static_cast<std::uint32_t>(lens[i] % 16);
+      const unsigned long long nb = m.nfull + ((pad && !dec) ? 1 : 0);
+      if (nb > 0xffffffffull) throw std::invalid_argument("message too large for the batch path");
+      m.nblocks = static_cast<std::uint32_t>(nb);
+      g += nb;
+      keys[i] = dec ? dec_key_words(rks + 176ull * i) : enc_key_words(rks + 176ull * i);
+    }
+    if (!d_in || !d_out) throw std::invalid_argument("null device buffer");
+    DevCtx& d = device(device_id);
+    DeviceGuard dg(device_id);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const bool check = dec && pad;
+    // descriptors: one device allocation, freed stream-ordered
+    const std::size_t msg_bytes = sizeof(BatchMsg) * n, key_bytes = sizeof(KeyWords) * n;
+    const std::size_t status_off = (msg_bytes + key_bytes + 255) & ~std::size_t(255);
+    const std::size_t total = status_off + (check ? 4ull * n : 0);
+    std::vector<std::uint8_t> host(total, 0);
+    std::memcpy(host.data(), msgs.data(), msg_bytes);
+    std::memcpy(host.data() + msg_bytes, keys.data(), key_bytes);
+    std::uint8_t* dd = nullptr;
+    PAES_CK(cudaMallocAsync(reinterpret_cast<void**>(&dd), total, s));
+    PAES_CK(cudaMemcpyAsync(dd, host.data(), status_off, cudaMemcpyHostToDevice, s));
+    BatchArgs a{};
+    a.in = static_cast<const std::uint8_t*>(d_in);
+    a.out = static_cast<std::uint8_t*>(d_out);
+    a.msgs = reinterpret_cast<const BatchMsg*>(dd);
+    a.keys = reinterpret_cast<const std::uint32_t*>(dd + msg_bytes);
+    a.status = check ? reinterpret_cast<std::uint32_t*>(dd + status_off) : nullptr;
+    a.total_blocks = g;
+    a.nmsg = n;
+    a.check_pad = check ? 1u : 0u;
+    PAES_CK(launch_batch(dec, a, d.sm_count, s));
+    if (check) {
+      std::vector<std::uint32_t> st(n);
+      PAES_CK(cudaMemcpyAsync(st.data(), dd + status_off, 4ull * n, cudaMemcpyDeviceToHost, s));
+      PAES_CK(cudaFreeAsync(dd, s));
+      PAES_CK(cudaStreamSynchronize(s));
+      bool bad = false;
+      for (uint32_t i = 0; i < n; ++i) {
+        const bool ok = st[i] != 0xffffffffu;
+        bad |= !ok;
+        if (out_lens) out_lens[i] = ok ? lens[i] - st[i] : UINT64_MAX;
+      }
+      if (bad) throw PaddingError("unpad: invalid pad bytes in one or more messages");
+    } else {
+      PAES_CK(cudaFreeAsync(dd, s));
+      if (out_lens)
+        for (uint32_t i = 0; i < n; ++i) out_lens[i] = static_cast<uint64_t>(msgs[i].nblocks) * 16;
+    }
+    return PAES_OK;
+  });
+}
+
+int paes_cuda_sweep(uint64_t seed, uint64_t size, uint8_t* out) {
+  return guarded([&] {
+    if (size && !out) throw std::invalid_argument("null buffer");
+    sweep(seed, size, out);
+    return PAES_OK;
+  });
+}
+
+int paes_cuda_batch_lengths(uint64_t seed, uint32_t n, uint64_t* lens) {
+  return guarded([&] {
+    if (n && !lens) throw std::invalid_argument("null buffer");
+    batch_lengths(seed, n, lens);
+    return PAES_OK;
+  });
+}
+
+int paes_cuda_counter_fill(uint64_t seed, uint64_t offset, uint64_t size, uint8_t* out) {
+  return guarded([&] {
+    if (offset % 8) throw std::invalid_argument("offset must be a multiple of 8");
+    if (size && !out) throw std::invalid_argument("null buffer");
+    uint64_t wi = offset / 8;
+    for (uint64_t off = 0; off < size; off += 8) {
+      const uint64_t w = counter_word(seed, wi++);
+      const uint64_t n = std::min<uint64_t>(8, size - off);
+      std::memcpy(out + off, &w, n);  // little-endian host
+    }
+    return PAES_OK;
+  });
+}
+
+int paes_cuda_counter_fill_device(uint64_t seed, uint64_t offset, uint64_t size, void* d_out, int device_id,
+                                  void* stream) {
+  return guarded([&] {
+    if (offset % 8 || size % 8) throw std::invalid_argument("offset and size must be multiples of 8");
+    if (size == 0) return PAES_OK;
+    if (!d_out || reinterpret_cast<std::uintptr_t>(d_out) % 16) throw std::invalid_argument("d_out must be 16-byte aligned");
+    DevCtx& d = device(device_id);
+    DeviceGuard g(device_id);
+    PAES_CK(launch_counter_fill(seed, offset / 8, size / 8, d_out, d.sm_count, static_cast<cudaStream_t>(stream)));
+    return PAES_OK;
+  });
+}
+
+int paes_cuda_checksum(const uint8_t* buf, uint64_t len, uint64_t base_word, uint64_t* out) {
+  return guarded([&] {
+    if (len % 8) throw std::invalid_argument("length must be a multiple of 8");
+    if ((len && !buf) || !out) throw std::invalid_argument("null buffer");
+    *out = checksum_words(buf, len, base_word);
+    return PAES_OK;
+  });
+}
+
+int paes_cuda_checksum_device(const void* d_buf, uint64_t len, uint64_t base_word, uint64_t* out, int device_id,
+                              void* stream) {
+  return guarded([&] {
+    if (len % 8) throw std::invalid_argument("length must be a multiple of 8");
+    if (!out) throw std::invalid_argument("null output");
+    if (len && (!d_buf || reinterpret_cast<std::uintptr_t>(d_buf) % 8)) throw std::invalid_argument("bad device buffer");
+    DevCtx& d = device(device_id);
+    DeviceGuard g(device_id);
+    std::lock_guard<std::mutex> lk(d.mu);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    PAES_CK(cudaMemsetAsync(d.d_acc, 0, 8, s));
+    PAES_CK(launch_checksum(d_buf, len / 8, base_word, d.d_acc, d.sm_count, s));
+    PAES_CK(cudaMemcpyAsync(d.h_acc, d.d_acc, 8, cudaMemcpyDeviceToHost, s));
+    PAES_CK(cudaStreamSynchronize(s));
+    *out = *d.h_acc;
+    return PAES_OK;
+  });
+}
+
+int paes_cuda_count_mismatch_device(const void* d_a, const void* d_b, uint64_t len, uint64_t* out, int device_id,
+                                    void* stream) {
+  return guarded([&] {
+    if (len % 16) throw std::invalid_argument("length must be a multiple of 16");
+    if (!out) throw std::invalid_argument("null output");
+    if (len && (!d_a || !d_b || (reinterpret_cast<std::uintptr_t>(d_a) | reinterpret_cast<std::uintptr_t>(d_b)) % 16))
+      throw std::invalid_argument("device buffers must be 16-byte aligned");
+    DevCtx& d = device(device_id);
+    DeviceGuard g(device_id);
+    std::lock_guard<std::mutex> lk(d.mu);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    PAES_CK(cudaMemsetAsync(d.d_acc, 0, 8, s));
+    PAES_CK(launch_mismatch(d_a, d_b, len / 16, d.d_acc, d.sm_count, s));
+    PAES_CK(cudaMemcpyAsync(d.h_acc, d.d_acc, 8, cudaMemcpyDeviceToHost, s));
+    PAES_CK(cudaStreamSynchronize(s));
+    *out = *d.h_acc;
+    return PAES_OK;
+  });
+}
+
+uint64_t paes_cuda_launch_count(void) { return launch_count(); }
+
+}  // extern "C"
+
+// ============================================================ file path
+namespace {
+
+struct Fd {
+  int fd = -1;
+  ~Fd() {
+    if (fd >= 0) ::close(fd);
+  }
+};
+
+struct IoFail {
+  std::string msg;
+};
+
+void pread_all(int fd, std::uint8_t* p, std::uint64_t n, std::uint64_t off, const std::string& path) {
+  std::uint64_t got = 0;
+  while (got < n) {
+    const ssize_t r = ::pread(fd, p + got, n - got, static_cast<off_t>(off + got));
+    if (r < 0 && errno == EINTR) continue;
+    if (r <= 0) throw IoFail{"short read: " + path};
+    got += static_cast<std::uint64_t>(r);
+  }
+}
+
+void pwrite_all(int fd, const std::uint8_t* p, std::uint64_t n, std::uint64_t off, const std::string& path) {
+  std::uint64_t put = 0;
+  while (put < n) {
+    const ssize_t r = ::pwrite(fd, p + put, n - put, static_cast<off_t>(off + put));
+    if (r < 0 && errno == EINTR) continue;
+    if (r <= 0) throw IoFail{"write failed: " + path};
+    put += static_cast<std::uint64_t>(r);
+  }
+}
+
+// One GPU's shard of a file job: pread into pinned slots, H2D, kernel, D2H
+// back into the same slot, pwrite -- all slots in flight at once.  Returns
+// the output bytes written (decrypt final: unpadded).
+std::uint64_t file_shard(DevCtx& d, const Range& r, int in_fd, int out_fd, std::uint64_t off, const KeyWords& kw,
+                         const std::string& in_path, const std::string& out_path) {
+  DeviceGuard g(d.id);
+  ensure_pipeline(d, true);
+  const std::uint64_t C = d.chunk;
+  const int S = static_cast<int>(d.st.size());
+  const std::uint64_t npieces = std::max<std::uint64_t>(1, (r.in_len + C - 1) / C);
+  std::vector<std::int64_t> pend_off(S, -1);
+  std::vector<std::uint64_t> pend_len(S, 0);
+  auto drain = [&](int s) {
+    if (pend_off[s] < 0) return;
+    PAES_CK(cudaEventSynchronize(d.ev[s]));
+    pwrite_all(out_fd, d.hbuf[s], pend_len[s], static_cast<std::uint64_t>(pend_off[s]), out_path);
+    pend_off[s] = -1;
+  };
+  std::uint64_t out_total = 0;
+  for (std::uint64_t k = 0; k < npieces; ++k) {
+    const int s = static_cast<int>(k % S);
+    drain(s);
+    const std::uint64_t poff = k * C;
+    const std::uint64_t len = std::min<std::uint64_t>(C, r.in_len - poff);
+    const bool last = k + 1 == npieces;
+    if (len) pread_all(in_fd, d.hbuf[s], len, off + poff, in_path);
+    EcbArgs a = make_args(r, d.dbuf[s], d.dbuf[s], len, last, kw, d.d_status);
+    if (len) PAES_CK(cudaMemcpyAsync(d.dbuf[s], d.hbuf[s], len, cudaMemcpyHostToDevice, d.st[s]));
+    if (a.check_pad) PAES_CK(cudaMemsetAsync(d.d_status, 0xff, 4, d.st[s]));
+    PAES_CK(launch_ecb(r.dec, a, d.sm_count, d.st[s]));
+    const std::uint64_t olen = a.nblocks * 16;
+    if (olen) PAES_CK(cudaMemcpyAsync(d.hbuf[s], d.dbuf[s], olen, cudaMemcpyDeviceToHost, d.st[s]));
+    if (last && a.check_pad) PAES_CK(cudaMemcpyAsync(d.h_status, d.d_status, 4, cudaMemcpyDeviceToHost, d.st[s]));
+    PAES_CK(cudaEventRecord(d.ev[s], d.st[s]));
+    pend_off[s] = static_cast<std::int64_t>(off + poff);
+    pend_len[s] = olen;
+    out_total = poff + olen;
+  }
+  for (int s = 0; s < S; ++s) drain(s);
+  if (r.check_pad) {
+    const std::uint32_t k = *d.h_status;
+    if (k == 0xffffffffu) throw PaddingError("unpad: invalid pad bytes");
+    out_total -= k;
+  }
+  return out_total;
+}
+
+}  // namespace
+
+extern "C" int paes_cuda_run_job(const char* input_path, const char* output_path, const uint8_t key[16],
+                                 uint32_t workers, int dir, paes_job_outcome* outcome) {
+  const auto t0 = std::chrono::steady_clock::now();
+  std::string tmp;
+  const int rc = guarded([&] {
+    if (!input_path || !output_path || !key) throw std::invalid_argument("null argument");
+    if (dir != PAES_ENCRYPT && dir != PAES_DECRYPT) throw std::invalid_argument("bad dir");
+    const bool dec = dir == PAES_DECRYPT;
+    const std::string in_path(input_path), out_path(output_path);
+    Fd in;
+    in.fd = ::open(input_path, O_RDONLY);
+    if (in.fd < 0) return fail(PAES_EIO, "cannot open input: " + in_path);
+    struct stat stt {};
+    if (::fstat(in.fd, &stt) != 0) return fail(PAES_EIO, "cannot stat input: " + in_path);
+    const std::uint64_t len = static_cast<std::uint64_t>(stt.st_size);
+    const auto devs = device_list(static_cast<int>(workers));
+    const auto plan = dec ? plan_decrypt_chunks(len, static_cast<unsigned>(devs.size()))
+                          : plan_chunks(len, static_cast<unsigned>(devs.size()));
+    std::uint8_t rk[176];
+    expand_key(key, rk);
+    const KeyWords kw = dec ? dec_key_words(rk) : enc_key_words(rk);
+    tmp = out_path + ".part." + std::to_string(::getpid());
+    Fd out;
+    out.fd = ::open(tmp.c_str(), O_WRONLY | O_CREAT | O_TRUNC, 0644);
+    if (out.fd < 0) return fail(PAES_EIO, "cannot open output: " + tmp);
+    std::vector<std::uint64_t> produced(plan.size(), 0);
+    std::vector<std::string> failures(plan.size());
+    auto work = [&](std::size_t i) {
+      const Chunk& c = plan[i];
+      Range r;
+      r.dec = dec;
+      r.in_len = c.raw_len;
+      r.pad = !dec && c.is_final;
+      r.check_pad = dec && c.is_final;
+      try {
+        DevCtx& d = device(devs[i]);
+        std::lock_guard<std::mutex> lk(d.mu);
+        produced[i] = file_shard(d, r, in.fd, out.fd, c.offset, kw, in_path, tmp);
+      } catch (const CudaFail& e) {
+        failures[i] = e.msg;
+      } catch (const IoFail& e) {
+        failures[i] = e.msg;
+      } catch (const std::exception& e) {
+        failures[i] = e.what();
+      }
+    };
+    if (plan.size() == 1) {
+      work(0);
+    } else {
+      std::vector<std::thread> pool;
+      for (std::size_t i = 0; i < plan.size(); ++i) pool.emplace_back(work, i);
+      for (auto& t : pool) t.join();
+    }
+    std::ostringstream failed;
+    bool any = false;
+    for (std::size_t i = 0; i < failures.size(); ++i) {
+      if (failures[i].empty()) continue;
+      failed << (any ? "; " : "") << "chunk " << i << ": " << failures[i];
+      any = true;
+    }
+    if (any) return fail(PAES_EWORKER, "worker failure: " + failed.str());
+    std::uint64_t total = 0;
+    for (auto p : produced) total += p;
+    if (::ftruncate(out.fd, static_cast<off_t>(total)) != 0) return fail(PAES_EIO, "truncate failed: " + tmp);
+    if (::rename(tmp.c_str(), output_path) != 0) return fail(PAES_EIO, "rename failed: " + out_path);
+    tmp.clear();
+    if (outcome) {
+      outcome->bytes_in = len;
+      outcome->bytes_out = total;
+      outcome->seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    }
+    return PAES_OK;
+  });
+  if (rc != PAES_OK && !tmp.empty()) ::unlink(tmp.c_str());  // no partial output (exec.cpp:86-91)
+  return rc;
+}

@@ -1,0 +1,337 @@
+"""Python face of the engine, mirroring the reference's ``_paes`` module.
+
+Same names, argument meaning and error behaviour as
+proj/python/paes_module.cpp (see the per-function citations), so the
+reference's own smoke tests read the same against this engine; every compute
+call goes through the C ABI (include/paes_cuda.h) into the sm_100a kernels.
+The only strategy is ``"gpu"`` (the reference's "sequential"/"threads"/
+"processes" CPU strategies are what this engine replaces).
+
+Exceptions (paes_module.cpp:153-155): PaddingError -> ValueError,
+WorkerError -> RuntimeError, IoError -> OSError.  CUDA failures raise
+GpuError (RuntimeError); invalid arguments raise ValueError as pybind11 maps
+std::invalid_argument.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from typing import Iterable, List
+
+from . import _native as N
+from ._native import DECRYPT, ENCRYPT
+
+BLOCK = 16
+
+
+class PaddingError(ValueError):
+    """Malformed PKCS#7 trailer (errors.hpp:24-27)."""
+
+
+class WorkerError(RuntimeError):
+    """One or more GPU shards failed; message names the chunk (errors.hpp:30-33)."""
+
+
+class IoError(OSError):
+    """File I/O failure (errors.hpp:13-21)."""
+
+
+class GpuError(RuntimeError):
+    """CUDA runtime failure or no usable device."""
+
+
+def _raise(rc: int) -> None:
+    if rc >= 0:
+        return
+    msg = N.last_error()
+    if rc == N.EBADMSG:
+        raise PaddingError(msg)
+    if rc == N.EINVAL:
+        raise ValueError(msg)
+    if rc == N.EWORKER:
+        raise WorkerError(msg)
+    if rc == N.EIO:
+        raise IoError(msg)
+    raise GpuError(f"{msg} (code {rc})")
+
+
+def _as_key(key: bytes) -> bytes:
+    key = bytes(key)
+    if len(key) != 16:
+        raise ValueError("key must be exactly 16 bytes")
+    return key
+
+
+class _InBuf:
+    """Borrow a read-only pointer to bytes-like data without copying."""
+
+    def __init__(self, data):
+        if isinstance(data, bytes):
+            self.keep = data
+            self.ptr = C.cast(C.c_char_p(data), C.c_void_p).value if data else None
+            self.n = len(data)
+            return
+        mv = memoryview(data).cast("B")
+        self.n = mv.nbytes
+        if self.n == 0:
+            self.keep, self.ptr = mv, None
+        elif mv.readonly:
+            self.keep = bytes(mv)
+            self.ptr = C.cast(C.c_char_p(self.keep), C.c_void_p).value
+        else:
+            arr = (C.c_uint8 * self.n).from_buffer(mv)
+            self.keep = (mv, arr)
+            self.ptr = C.addressof(arr)
+
+
+def round_keys(key: bytes) -> bytes:
+    """176-byte expanded schedule (RoundKeySchedule, aes.cpp:151-180)."""
+    key = _as_key(key)
+    rk = (C.c_uint8 * 176)()
+    _raise(N.load().paes_cuda_expand_key(key, rk))
+    return bytes(rk)
+
+
+def expand_key(key: bytes) -> List[bytes]:
+    """11 round keys (paes_module.cpp:59-68)."""
+    rk = round_keys(key)
+    return [rk[16 * r:16 * r + 16] for r in range(11)]
+
+
+# ---------------------------------------------------------------- bulk ECB
+def ecb(direction: int, data, key: bytes, ngpus: int = 0) -> bytes:
+    """aes::encrypt_ecb / decrypt_ecb (aes.hpp:86-89) over host memory."""
+    rk = round_keys(key)
+    src = _InBuf(data)
+    out = C.create_string_buffer(max(src.n, 1))
+    _raise(N.load().paes_cuda_ecb(direction, src.ptr, out, src.n, rk, ngpus))
+    return out.raw[: src.n]
+
+
+def encrypt_ecb(data, key: bytes, ngpus: int = 0) -> bytes:
+    return ecb(ENCRYPT, data, key, ngpus)
+
+
+def decrypt_ecb(data, key: bytes, ngpus: int = 0) -> bytes:
+    return ecb(DECRYPT, data, key, ngpus)
+
+
+def encrypt_block(block: bytes, key: bytes) -> bytes:
+    """paes_module.cpp:70-75 (one block through the GPU path)."""
+    if len(block) != 16:
+        raise ValueError("block must be exactly 16 bytes")
+    return ecb(ENCRYPT, bytes(block), key, 1)
+
+
+def decrypt_block(block: bytes, key: bytes) -> bytes:
+    if len(block) != 16:
+        raise ValueError("block must be exactly 16 bytes")
+    return ecb(DECRYPT, bytes(block), key, 1)
+
+
+# ---------------------------------------------------------------- chunks
+def chunk(direction: int, data, is_final: bool, key: bytes, ngpus: int = 0) -> bytes:
+    """encrypt_chunk / decrypt_chunk (exec.hpp:61-65) over host memory."""
+    rk = round_keys(key)
+    src = _InBuf(data)
+    cap = src.n + (BLOCK if (direction == ENCRYPT and is_final) else 0)
+    out = C.create_string_buffer(max(cap, 1))
+    olen = C.c_uint64()
+    _raise(N.load().paes_cuda_chunk(direction, src.ptr, src.n, int(bool(is_final)), rk, out, C.byref(olen), ngpus))
+    return out.raw[: olen.value]
+
+
+def encrypt_chunk(data, is_final: bool, key: bytes, ngpus: int = 0) -> bytes:
+    return chunk(ENCRYPT, data, is_final, key, ngpus)
+
+
+def decrypt_chunk(data, is_final: bool, key: bytes, ngpus: int = 0) -> bytes:
+    return chunk(DECRYPT, data, is_final, key, ngpus)
+
+
+def encrypt_bytes(data, key: bytes) -> bytes:
+    """ECB over the PKCS#7-padded input (paes_module.cpp:84-88)."""
+    return chunk(ENCRYPT, data, True, key)
+
+
+def decrypt_bytes(data, key: bytes) -> bytes:
+    """paes_module.cpp:90-93: raises PaddingError (ValueError) on a bad trailer."""
+    return chunk(DECRYPT, data, True, key)
+
+
+# ---------------------------------------------------------------- host rules
+def pkcs7_pad(data) -> bytes:
+    """pad_final (chunk.cpp:83-88)."""
+    src = _InBuf(data)
+    out = C.create_string_buffer(src.n + BLOCK)
+    n = N.load().paes_cuda_pad_final(src.ptr, src.n, out)
+    _raise(n)
+    return out.raw[:n]
+
+
+def pkcs7_unpad(data) -> bytes:
+    """unpad_final (chunk.cpp:90-100)."""
+    src = _InBuf(data)
+    n = N.load().paes_cuda_unpad_final(src.ptr, src.n)
+    _raise(n)
+    return bytes(memoryview(data).cast("B")[:n]) if not isinstance(data, bytes) else data[:n]
+
+
+def _plan(fn, total_len: int, workers: int):
+    L = N.load()
+    cap = max(1, min(int(workers), int(total_len) // 16 + 1))
+    arr = (N.ChunkSpec * cap)()
+    n = getattr(L, fn)(total_len, workers, arr, cap)
+    _raise(n)
+    return [{"offset": c.offset, "raw_len": c.raw_len, "padded_len": c.padded_len, "is_final": bool(c.is_final)}
+            for c in arr[:n]]
+
+
+def plan_chunks(total_len: int, workers: int):
+    """plan_chunks (chunk.cpp:27-55) -- also the multi-GPU shard rule."""
+    if workers < 0:
+        raise ValueError("workers must be >= 1")
+    return _plan("paes_cuda_plan_chunks", total_len, workers)
+
+
+def plan_decrypt_chunks(cipher_len: int, workers: int):
+    """plan_decrypt_chunks (chunk.cpp:57-81)."""
+    if workers < 0:
+        raise ValueError("workers must be >= 1")
+    return _plan("paes_cuda_plan_decrypt_chunks", cipher_len, workers)
+
+
+def reject_outliers(samples: Iterable[float]) -> List[float]:
+    """Median/MAD filter of the bench harness (bench.cpp:49-79), restated."""
+    s = [float(x) for x in samples]
+    if not s:
+        raise ValueError("reject_outliers: no samples")
+    n = len(s)
+
+    def median(v):
+        v = sorted(v)
+        return v[n // 2] if n % 2 else 0.5 * (v[n // 2 - 1] + v[n // 2])
+
+    m = median(s)
+    devs = [abs(x - m) for x in s]
+    mad = median(devs)
+    thr = 3.0 * mad if mad > 0.0 else 0.01 * abs(m)
+    keep = [i for i in range(n) if devs[i] <= thr]
+    floor = (n + 1) // 2
+    if len(keep) < floor:
+        order = sorted(range(n), key=lambda i: devs[i])  # stable: ties keep index order
+        keep = sorted(order[:floor])
+    return [s[i] for i in keep]
+
+
+# ---------------------------------------------------------------- files
+def _job(direction: int, input: str, output: str, key: bytes, workers: int, strategy: str, worker_exe: str):
+    if strategy != "gpu":
+        raise ValueError("strategy must be gpu (this engine replaces the sequential/threads/processes CPU strategies)")
+    if workers < 0:
+        raise ValueError("workers must be >= 0")
+    key = _as_key(key)
+    o = N.JobOutcome()
+    _raise(N.load().paes_cuda_run_job(os.fsencode(input), os.fsencode(output), key, workers, direction, C.byref(o)))
+    return {"bytes_in": o.bytes_in, "bytes_out": o.bytes_out, "seconds": o.seconds}
+
+
+def encrypt_file(input: str, output: str, key: bytes, workers: int = 1, strategy: str = "gpu", worker_exe: str = ""):
+    """run_job(Encrypt) with ExecStrategy "gpu" (paes_module.cpp:95-109); workers = GPUs (0 = all)."""
+    return _job(ENCRYPT, input, output, key, workers, strategy, worker_exe)
+
+
+def decrypt_file(input: str, output: str, key: bytes, workers: int = 1, strategy: str = "gpu", worker_exe: str = ""):
+    return _job(DECRYPT, input, output, key, workers, strategy, worker_exe)
+
+
+# ---------------------------------------------------------------- device side
+def device_count() -> int:
+    return int(N.load().paes_cuda_device_count())
+
+
+def set_devices(ids) -> None:
+    ids = list(ids)
+    arr = (C.c_int * max(len(ids), 1))(*ids)
+    _raise(N.load().paes_cuda_set_devices(arr, len(ids)))
+
+
+def set_pipeline(chunk_bytes: int = 0, streams: int = 0) -> None:
+    _raise(N.load().paes_cuda_set_pipeline(chunk_bytes, streams))
+
+
+def ecb_device(direction: int, d_in: int, d_out: int, nbytes: int, rk: bytes, device: int = 0, stream: int = 0):
+    """Device-resident ECB on raw pointers (asynchronous on `stream`)."""
+    _raise(N.load().paes_cuda_ecb_device(direction, d_in, d_out, nbytes, rk, device, stream or None))
+
+
+def chunk_device(direction: int, d_in: int, nbytes: int, is_final: bool, rk: bytes, d_out: int, device: int = 0,
+                 stream: int = 0) -> int:
+    olen = C.c_uint64()
+    _raise(N.load().paes_cuda_chunk_device(direction, d_in, nbytes, int(bool(is_final)), rk, d_out, C.byref(olen),
+                                           device, stream or None))
+    return olen.value
+
+
+def ecb_batch(direction: int, d_in: int, d_out: int, in_off, out_off, lens, rks: bytes, pad: bool, device: int = 0,
+              stream: int = 0):
+    n = len(lens)
+    A = C.c_uint64 * max(n, 1)
+    olens = A()
+    _raise(N.load().paes_cuda_ecb_batch(direction, d_in, d_out, A(*in_off), A(*out_off), A(*lens), rks, n,
+                                        int(bool(pad)), olens, device, stream or None))
+    return list(olens[:n])
+
+
+def sweep(seed: int, size: int) -> bytes:
+    """generate_sweep_file (bench.cpp:109-125) into memory."""
+    out = C.create_string_buffer(max(size, 1))
+    _raise(N.load().paes_cuda_sweep(seed, size, out))
+    return out.raw[:size]
+
+
+def sweep_into(seed: int, size: int, ptr: int) -> None:
+    _raise(N.load().paes_cuda_sweep(seed, size, ptr))
+
+
+def batch_lengths(seed: int, n: int) -> List[int]:
+    arr = (C.c_uint64 * max(n, 1))()
+    _raise(N.load().paes_cuda_batch_lengths(seed, n, arr))
+    return list(arr[:n])
+
+
+def counter_fill(seed: int, offset: int, size: int) -> bytes:
+    out = C.create_string_buffer(max(size, 1))
+    _raise(N.load().paes_cuda_counter_fill(seed, offset, size, out))
+    return out.raw[:size]
+
+
+def counter_fill_device(seed: int, offset: int, size: int, d_out: int, device: int = 0, stream: int = 0) -> None:
+    _raise(N.load().paes_cuda_counter_fill_device(seed, offset, size, d_out, device, stream or None))
+
+
+def checksum(data, base_word: int = 0) -> int:
+    src = _InBuf(data)
+    out = C.c_uint64()
+    _raise(N.load().paes_cuda_checksum(src.ptr, src.n, base_word, C.byref(out)))
+    return out.value
+
+
+def checksum_device(d_buf: int, nbytes: int, base_word: int = 0, device: int = 0, stream: int = 0) -> int:
+    out = C.c_uint64()
+    _raise(N.load().paes_cuda_checksum_device(d_buf, nbytes, base_word, C.byref(out), device, stream or None))
+    return out.value
+
+
+def count_mismatch_device(d_a: int, d_b: int, nbytes: int, device: int = 0, stream: int = 0) -> int:
+    out = C.c_uint64()
+    _raise(N.load().paes_cuda_count_mismatch_device(d_a, d_b, nbytes, C.byref(out), device, stream or None))
+    return out.value
+
+
+def launch_count() -> int:
+    return int(N.load().paes_cuda_launch_count())
+
+
+def version() -> str:
+    return N.load().paes_cuda_version().decode()

@@ -1,0 +1,392 @@
+"""GPU parity: the sm_100a path (through the C ABI) vs the oracle and the
+reference's own golden vectors.  Bit-exact everywhere (integer/byte work).
+
+Small and medium sizes compare against the oracle / golden.json directly;
+full BASELINE.json sizes compare against digests.json (computed by the
+reference's own paes_core, tests/golden/make_digests.py) plus size-independent
+properties (decrypt(encrypt(x)) == x, additive position-keyed checksums).
+"""
+from __future__ import annotations
+
+import hashlib
+import os
+import random
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+MiB = 1 << 20
+GiB = 1 << 30
+
+
+def _torch():
+    import torch
+
+    return torch
+
+
+def dev_from_bytes(data: bytes, extra: int = 0, offset: int = 0):
+    """Device uint8 tensor holding `data` at byte `offset`, with `extra` spare bytes."""
+    torch = _torch()
+    t = torch.zeros(offset + len(data) + extra + 16, dtype=torch.uint8, device="cuda")
+    if data:
+        t[offset:offset + len(data)] = torch.frombuffer(bytearray(data), dtype=torch.uint8).cuda()
+    return t
+
+
+def to_bytes(t, start: int, n: int) -> bytes:
+    return t[start:start + n].cpu().numpy().tobytes()
+
+
+# ------------------------------------------------------------ KATs / golden
+def test_block_kats(paes, gpu, golden):
+    """FIPS-197 B and C.1 + zero-key decrypt snapshot (test_aes.cpp:255-292)."""
+    for kat in golden["block_kats"]:
+        key, pt = bytes.fromhex(kat["key"]), bytes.fromhex(kat["pt"])
+        ct = paes.encrypt_block(pt, key)
+        assert ct.hex() == kat["ct"]
+        assert paes.decrypt_block(ct, key) == pt
+        assert paes.decrypt_block(pt, key).hex() == kat["dec_of_pt"]
+    assert paes.decrypt_block(bytes(16), bytes(16)).hex() == "140f0f1011b5223d79587717ffd9ec3a"
+
+
+def test_encrypt_bytes_golden(paes, gpu, golden):
+    """Always-pad chunk path vs vectors from the reference's _paes.encrypt_bytes."""
+    for e in golden["bytes"]:
+        key, pt = bytes.fromhex(e["key"]), bytes.fromhex(e["pt"])
+        ct = paes.encrypt_bytes(pt, key)
+        assert len(ct) == (len(pt) // 16 + 1) * 16
+        if "ct" in e:
+            assert ct.hex() == e["ct"], e["len"]
+        else:
+            assert hashlib.sha256(ct).hexdigest() == e["ct_sha256"], e["len"]
+        assert paes.decrypt_bytes(ct, key) == pt
+
+
+def test_wrong_key_raises_padding_error(paes, gpu, golden):
+    """test_smoke.py:28-31; the reference outcome is recorded per case."""
+    for w in golden["wrong_key"]:
+        ct = bytes.fromhex(w["ct"])
+        if w["outcome"] == "PaddingError":
+            with pytest.raises(ValueError):
+                paes.decrypt_bytes(ct, bytes.fromhex(w["bad_key"]))
+            with pytest.raises(paes.PaddingError):
+                paes.decrypt_bytes(ct, bytes.fromhex(w["bad_key"]))
+        else:
+            paes.decrypt_bytes(ct, bytes.fromhex(w["bad_key"]))
+
+
+def test_ecb_property_and_length_errors(paes, gpu, orc):
+    """test_aes.cpp:294-312: 16 zero blocks -> 16 identical blocks; 15 bytes throws."""
+    key = bytes(range(16))
+    out = paes.encrypt_ecb(bytes(256), key)
+    one = orc.encrypt_block(bytes(16), key)
+    assert out == one * 16
+    assert paes.decrypt_ecb(out, key) == bytes(256)
+    with pytest.raises(ValueError):
+        paes.encrypt_ecb(bytes(15), key)
+    with pytest.raises(ValueError):
+        paes.encrypt_chunk(bytes(17), False, key)
+    with pytest.raises(paes.PaddingError):
+        paes.decrypt_bytes(b"", key)
+    with pytest.raises(ValueError):
+        paes.decrypt_chunk(bytes(17), False, key)
+
+
+def test_empty_and_ragged_vs_oracle(paes, gpu, orc):
+    rnd = random.Random(11)
+    for n in list(range(0, 70)) + [255, 256, 257, 4095, 4096, 4097, 65535, 65536, 65537, 100001]:
+        key = bytes(rnd.getrandbits(8) for _ in range(16))
+        data = os.urandom(n)
+        ct = paes.encrypt_bytes(data, key)
+        assert ct == orc.encrypt_chunk(data, True, key), n
+        assert paes.decrypt_bytes(ct, key) == data
+        if n % 16 == 0:
+            raw = paes.encrypt_chunk(data, False, key)
+            assert raw == orc.ecb(0, data, key)
+            assert paes.decrypt_chunk(raw, False, key) == data
+
+
+def test_decrypt_random_ciphertext_vs_oracle(paes, gpu, orc):
+    """Non-final decrypt of arbitrary blocks == the reference's straightforward inverse."""
+    key = os.urandom(16)
+    data = os.urandom(16 * 4099)
+    assert paes.decrypt_ecb(data, key) == orc.ecb(1, data, key)
+
+
+def test_pipeline_piece_boundaries(paes, gpu, orc):
+    """Host pipeline with a tiny staging chunk: many pieces, pad on the last one."""
+    paes.set_pipeline(4096, 3)
+    try:
+        key = os.urandom(16)
+        for n in [0, 1, 15, 16, 4095, 4096, 4097, 8192, 8192 + 7, 3 * 4096, 3 * 4096 + 15, 40000]:
+            data = os.urandom(n)
+            ct = paes.encrypt_bytes(data, key)
+            assert ct == orc.encrypt_chunk(data, True, key), n
+            assert paes.decrypt_bytes(ct, key) == data
+    finally:
+        paes.set_pipeline(32 * MiB, 4)
+
+
+def test_in_place_host(paes, gpu, orc):
+    """in and out may alias exactly (aes.hpp:84-85)."""
+    import ctypes as C
+
+    from paper_1403_7295_b200 import _native as N
+
+    key = os.urandom(16)
+    data = os.urandom(16 * 1000)
+    buf = C.create_string_buffer(data, len(data))
+    rk = paes.round_keys(key)
+    assert N.load().paes_cuda_ecb(0, buf, buf, len(data), rk, 1) == 0
+    assert buf.raw[: len(data)] == orc.ecb(0, data, key)
+
+
+# ------------------------------------------------------------ device API
+def test_chunk_device_tails_alignment_inplace(paes, gpu, orc):
+    torch = _torch()
+    key = os.urandom(16)
+    rk = paes.round_keys(key)
+    for n in [0, 1, 7, 15, 16, 17, 31, 33, 511, 512, 513, 16 * 1024 * 3 + 9]:
+        data = os.urandom(n)
+        want = orc.encrypt_chunk(data, True, key)
+        for off in (0, 1, 8):  # unaligned device pointers take the byte path
+            src = dev_from_bytes(data, offset=off)
+            dst = torch.zeros(len(want) + off + 16, dtype=torch.uint8, device="cuda")
+            m = paes.chunk_device(0, src.data_ptr() + off, n, True, rk, dst.data_ptr() + off)
+            assert m == len(want)
+            assert to_bytes(dst, off, m) == want, (n, off)
+            back = torch.zeros_like(dst)
+            k = paes.chunk_device(1, dst.data_ptr() + off, m, True, rk, back.data_ptr() + off)
+            assert k == n and to_bytes(back, off, n) == data
+        # in place: encrypt then decrypt in the same buffer
+        buf = dev_from_bytes(data, extra=16)
+        m = paes.chunk_device(0, buf.data_ptr(), n, True, rk, buf.data_ptr())
+        assert to_bytes(buf, 0, m) == want
+        k = paes.chunk_device(1, buf.data_ptr(), m, True, rk, buf.data_ptr())
+        assert k == n and to_bytes(buf, 0, n) == data
+    torch.cuda.synchronize()
+
+
+def test_chunk_device_wrong_key(paes, gpu):
+    torch = _torch()
+    key = os.urandom(16)
+    ct = paes.encrypt_bytes(os.urandom(1000), key)
+    src = dev_from_bytes(ct)
+    dst = torch.zeros_like(src)
+    bad = paes.round_keys(bytes([key[0] ^ 0x5A]) + key[1:])
+    with pytest.raises(paes.PaddingError):
+        paes.chunk_device(1, src.data_ptr(), len(ct), True, bad, dst.data_ptr())
+
+
+def test_ecb_device_on_torch_stream(paes, gpu, orc):
+    torch = _torch()
+    key = os.urandom(16)
+    rk = paes.round_keys(key)
+    data = os.urandom(16 * 70001)
+    src = dev_from_bytes(data)
+    dst = torch.empty_like(src)
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        paes.ecb_device(0, src.data_ptr(), dst.data_ptr(), len(data), rk, 0, s.cuda_stream)
+    s.synchronize()
+    assert to_bytes(dst, 0, len(data)) == orc.ecb(0, data, key)
+
+
+def test_launch_count_advances(paes, gpu):
+    before = paes.launch_count()
+    paes.encrypt_bytes(b"x" * 100, bytes(16))
+    assert paes.launch_count() > before
+
+
+def test_more_gpus_than_visible_is_an_error(paes, gpu):
+    with pytest.raises(paes.GpuError):
+        paes.encrypt_ecb(bytes(16), bytes(16), ngpus=paes.device_count() + 1)
+
+
+# ------------------------------------------------------------ files (run_job "gpu")
+def test_file_roundtrip_and_failure(paes, gpu, orc, tmp_path):
+    """test_smoke.py:55-69 and test_exec.cpp:235-267 with strategy "gpu"."""
+    key = bytes.fromhex("000102030405060708090a0b0c0d0e0f")
+    data = os.urandom(100_000)
+    src = tmp_path / "plain.bin"
+    src.write_bytes(data)
+    enc = paes.encrypt_file(str(src), str(tmp_path / "c.bin"), key, workers=1)
+    assert enc["bytes_in"] == len(data)
+    assert enc["bytes_out"] == (len(data) // 16 + 1) * 16
+    assert (tmp_path / "c.bin").read_bytes() == orc.encrypt_chunk(data, True, key)
+    dec = paes.decrypt_file(str(tmp_path / "c.bin"), str(tmp_path / "p.bin"), key, workers=1)
+    assert dec["bytes_out"] == len(data)
+    assert (tmp_path / "p.bin").read_bytes() == data
+    # empty file -> one pad block
+    (tmp_path / "e.bin").write_bytes(b"")
+    assert paes.encrypt_file(str(tmp_path / "e.bin"), str(tmp_path / "e.enc"), key)["bytes_out"] == 16
+    # wrong key: WorkerError naming the final chunk, no output left behind
+    bad = bytes([key[0] ^ 1]) + key[1:]
+    with pytest.raises(paes.WorkerError, match="chunk 0"):
+        paes.decrypt_file(str(tmp_path / "c.bin"), str(tmp_path / "bad.bin"), bad, workers=1)
+    assert not (tmp_path / "bad.bin").exists()
+    assert not any(p.name.startswith("bad.bin.part") for p in tmp_path.iterdir())
+    with pytest.raises(OSError):
+        paes.encrypt_file(str(tmp_path / "missing.bin"), str(tmp_path / "x.bin"), key)
+    with pytest.raises(paes.PaddingError):
+        paes.decrypt_file(str(tmp_path / "e.bin"), str(tmp_path / "x.bin"), key)
+
+
+def test_file_pipeline_many_pieces(paes, gpu, orc, tmp_path):
+    paes.set_pipeline(64 * 1024, 3)
+    try:
+        key = os.urandom(16)
+        data = os.urandom(1_000_007)
+        (tmp_path / "a").write_bytes(data)
+        paes.encrypt_file(str(tmp_path / "a"), str(tmp_path / "b"), key)
+        assert (tmp_path / "b").read_bytes() == orc.encrypt_chunk(data, True, key, threads=4)
+        paes.decrypt_file(str(tmp_path / "b"), str(tmp_path / "c"), key)
+        assert (tmp_path / "c").read_bytes() == data
+    finally:
+        paes.set_pipeline(32 * MiB, 4)
+
+
+# ------------------------------------------------------------ BASELINE.json configs
+def test_config1_64mib_roundtrip(paes, gpu, digests):
+    """Config 1: sweep(0, 64 MiB) under key sweep(0,16); SURVEY.md A.5 digests."""
+    d = digests["cfg1"]
+    pt = paes.sweep(0, 64 * MiB)
+    key = paes.sweep(0, 16)
+    assert key.hex() == d["key"] == "4c287f4282c15e6cfda0c041590ebc2a"
+    assert hashlib.sha256(pt).hexdigest() == d["pt_sha256"]
+    ct = paes.encrypt_bytes(pt, key)
+    assert len(ct) == 64 * MiB + 16
+    assert hashlib.sha256(ct).hexdigest() == d["ct_sha256"] == \
+        "2d8284614df3ca943d7e0ac3bedac30a15ff45797dddbaf734a3a454245b74d0"
+    assert hashlib.sha256(paes.encrypt_ecb(pt, key)).hexdigest() == d["raw_ecb_sha256"]
+    assert paes.decrypt_bytes(ct, key) == pt
+
+
+def test_config2_1gib_decrypt(paes, gpu, digests):
+    """Config 2: decrypt of the reference's 1 GiB ciphertext (device-resident)."""
+    torch = _torch()
+    d = digests["cfg2"]
+    key = paes.sweep(1, 16)
+    rk = paes.round_keys(key)
+    n = (1 << 30) - 16
+    host = np.empty(n, dtype=np.uint8)
+    paes.sweep_into(1, n, host.ctypes.data)
+    assert hashlib.sha256(memoryview(host)).hexdigest() == d["pt_sha256"]
+    pt = torch.from_numpy(host).cuda()
+    ct = torch.empty(GiB, dtype=torch.uint8, device="cuda")
+    assert paes.chunk_device(0, pt.data_ptr(), n, True, rk, ct.data_ptr()) == GiB
+    assert hashlib.sha256(memoryview(ct.cpu().numpy())).hexdigest() == d["ct_sha256"]
+    back = torch.empty(GiB, dtype=torch.uint8, device="cuda")
+    assert paes.chunk_device(1, ct.data_ptr(), GiB, True, rk, back.data_ptr()) == n
+    assert paes.count_mismatch_device(back.data_ptr(), pt.data_ptr(), n - n % 16) == 0
+    assert to_bytes(back, n - n % 16, n % 16) == host[n - n % 16:].tobytes()
+
+
+@pytest.mark.slow
+def test_config3_size_sweep(paes, gpu, digests):
+    """Config 3: 1 KiB .. 4 GiB + 7-byte tail (nine 0x09 pad bytes)."""
+    torch = _torch()
+    d = digests["cfg3"]
+    key = paes.sweep(2, 16)
+    rk = paes.round_keys(key)
+    for e in d["sizes"]:
+        n = e["len"]
+        host = np.empty(n, dtype=np.uint8)
+        paes.sweep_into(2, n, host.ctypes.data)
+        if n <= 256 * MiB + 7:  # host API (E2E path)
+            ct = paes.encrypt_bytes(memoryview(host), key)
+            assert len(ct) == e["ct_len"]
+            assert hashlib.sha256(ct).hexdigest() == e["ct_sha256"], n
+        else:  # device-resident path for 4 GiB
+            src = torch.from_numpy(host).cuda()
+            del host
+            dst = torch.empty(e["ct_len"], dtype=torch.uint8, device="cuda")
+            assert paes.chunk_device(0, src.data_ptr(), n, True, rk, dst.data_ptr()) == e["ct_len"]
+            out = dst.cpu().numpy()
+            assert out[-16:].tobytes().hex() == e["ct_last16"]
+            assert hashlib.sha256(memoryview(out)).hexdigest() == e["ct_sha256"]
+            del src, dst, out
+            torch.cuda.empty_cache()
+
+
+@pytest.mark.slow
+def test_config4_64gib_device_generated(paes, gpu, digests):
+    """Config 4: 64 GiB counter stream generated on device, encrypted, checked by
+    the reference's full-stream checksums + sampled windows + round trip."""
+    torch = _torch()
+    d = digests["cfg4"]
+    total = d["len"]
+    key = paes.sweep(3, 16)
+    assert key.hex() == d["key"]
+    rk = paes.round_keys(key)
+    free, _ = torch.cuda.mem_get_info()
+    if free < 2 * total + GiB:
+        pytest.fail(f"config 4 needs {2 * total + GiB} bytes of HBM, {free} free")
+    pt = torch.empty(total, dtype=torch.uint8, device="cuda")
+    ct = torch.empty(total + 16, dtype=torch.uint8, device="cuda")
+    paes.counter_fill_device(3, 0, total, pt.data_ptr())
+    assert paes.checksum_device(pt.data_ptr(), total, 0) == d["pt_checksum"]
+    assert paes.chunk_device(0, pt.data_ptr(), total, True, rk, ct.data_ptr()) == total + 16
+    assert paes.checksum_device(ct.data_ptr(), total + 16, 0) == d["ct_checksum"]
+    assert to_bytes(ct, total, 16).hex() == d["pad_block"]
+    W = d["window"]
+    for off, h in d["window_sha256"].items():
+        off = int(off)
+        assert hashlib.sha256(to_bytes(ct, off, W)).hexdigest() == h, off
+    # round trip in place over the plaintext buffer
+    assert paes.chunk_device(1, ct.data_ptr(), total + 16, True, rk, pt.data_ptr()) == total
+    assert paes.checksum_device(pt.data_ptr(), total, 0) == d["pt_checksum"]
+    del pt, ct
+    torch.cuda.empty_cache()
+
+
+def _cfg5_inputs(paes, n, lens):
+    in_off, out_off, o_in, o_out = [], [], 0, 0
+    for L in lens:
+        in_off.append(o_in)
+        out_off.append(o_out)
+        o_in += L + 16  # room for the decrypted pad block on the way back
+        o_out += L + 16
+    host = np.full(o_in, 0x10, dtype=np.uint8)
+    keys = bytearray()
+    for i in range(n):
+        seed = (4 << 32) + i
+        paes.sweep_into(seed, lens[i], host.ctypes.data + in_off[i])
+        keys += paes.round_keys(paes.sweep(seed, 16))
+    return host, in_off, out_off, bytes(keys), o_out
+
+
+@pytest.mark.slow
+def test_config5_batch_4096_messages(paes, gpu, digests):
+    """Config 5: 4096 messages, per-message keys, one fused launch per direction."""
+    torch = _torch()
+    d = digests["cfg5"]
+    n = d["n"]
+    lens = paes.batch_lengths(4, n)
+    assert hashlib.sha256(np.array(lens, dtype=np.uint64).tobytes()).hexdigest() == d["lens_sha256"]
+    host, in_off, out_off, rks, out_total = _cfg5_inputs(paes, n, lens)
+    src = torch.from_numpy(host).cuda()
+    dst = torch.empty(out_total, dtype=torch.uint8, device="cuda")
+    before = paes.launch_count()
+    olens = paes.ecb_batch(0, src.data_ptr(), dst.data_ptr(), in_off, out_off, lens, rks, True)
+    assert paes.launch_count() - before == 1
+    assert olens == [L + 16 for L in lens]
+    out = dst.cpu().numpy()
+    hc = hashlib.sha256()
+    for i in range(n):
+        c = out[out_off[i]:out_off[i] + lens[i] + 16]
+        hc.update(memoryview(c))
+        assert hashlib.sha256(memoryview(c)).hexdigest()[:16] == d["ct_msg_sha256_16"][i], i
+    assert hc.hexdigest() == d["ct_concat_sha256"]
+    back = torch.zeros_like(src)
+    plens = paes.ecb_batch(1, dst.data_ptr(), back.data_ptr(), out_off, in_off, [L + 16 for L in lens], rks, True)
+    assert plens == lens
+    assert paes.count_mismatch_device(back.data_ptr(), src.data_ptr(), src.numel()) == 0
+    # a corrupted key for one message -> PaddingError, the others still reported
+    bad = bytearray(rks)
+    bad[176 * 7 + 160] ^= 0xFF
+    with pytest.raises(paes.PaddingError):
+        paes.ecb_batch(1, dst.data_ptr(), back.data_ptr(), out_off, in_off, [L + 16 for L in lens], bytes(bad), True)
