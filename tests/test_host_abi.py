@@ -1,0 +1,205 @@
+"""CPU-only: the C-ABI library loads and exports every declared symbol, and
+its host-side rules (key expansion, planner/sharder, PKCS#7, seeded inputs,
+checksums) match the oracle and the reference's golden vectors.  No kernel
+is launched here."""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import random
+import re
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def declared_symbols():
+    src = open(os.path.join(ROOT, "include", "paes_cuda.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(paes_cuda_\w+)\s*\(", src)))
+
+
+def test_library_exports_every_declared_symbol(lib):
+    syms = declared_symbols()
+    assert len(syms) >= 20
+    for s in syms:
+        assert hasattr(lib, s), s
+    from paper_1403_7295_b200 import _native
+
+    assert sorted(n for n, _, _ in _native.SIGNATURES) == syms
+
+
+def test_library_is_sm100a_and_not_a_fallback():
+    from paper_1403_7295_b200 import _native
+
+    path = _native.lib_path()
+    blob = open(path, "rb").read()
+    assert b"sm_100a" in blob  # embedded cubin for the right arch
+    import subprocess
+
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "-lelf", path], capture_output=True, text=True)
+    if out.returncode == 0:
+        assert "sm_100a" in out.stdout
+
+
+def test_no_oracle_in_product():
+    """The product package never imports/links the oracle."""
+    pkg = os.path.join(ROOT, "paper_1403_7295_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh", ".cpp", ".hpp")):
+                text = open(os.path.join(dirpath, f), errors="ignore").read()
+                assert "import oracle" not in text and "liboracle" not in text and "libpaes_ref" not in text, f
+
+
+def test_version(paes):
+    assert "sm_100a" in paes.version()
+
+
+def test_expand_key_matches_golden(paes, golden):
+    for e in golden["key_schedules"]:
+        assert paes.round_keys(bytes.fromhex(e["key"])).hex() == e["rk"]
+    keys = paes.expand_key(bytes.fromhex("000102030405060708090a0b0c0d0e0f"))
+    assert len(keys) == 11 and keys[0].hex() == "000102030405060708090a0b0c0d0e0f"  # test_smoke.py:21-25
+    assert paes.expand_key(bytes(16))[1].hex() == "62636363" * 4
+    with pytest.raises(ValueError):
+        paes.round_keys(b"short")
+
+
+def test_random_key_schedules_vs_oracle(paes, orc):
+    rnd = random.Random(9)
+    for _ in range(200):
+        k = bytes(rnd.randrange(256) for _ in range(16))
+        assert paes.round_keys(k) == orc.expand_key(k)
+
+
+def test_plan_chunks_examples(paes, golden):
+    """test_chunk.cpp:57-103 + golden grid from the reference's _paes.plan_chunks."""
+    assert [c["raw_len"] for c in paes.plan_chunks(1000, 4)] == [256, 256, 256, 232]
+    assert paes.plan_chunks(1000, 4)[-1]["padded_len"] == 240
+    assert len(paes.plan_chunks(16, 33)) == 1 and len(paes.plan_chunks(17, 33)) == 2
+    assert paes.plan_chunks(0, 33) == [{"offset": 0, "raw_len": 0, "padded_len": 16, "is_final": True}]
+    assert len(paes.plan_chunks(1024, 65)) == 64  # chunk cap = data blocks (Appendix C.1)
+    for e in golden["plans"]:
+        got = [[c["offset"], c["raw_len"], c["padded_len"], c["is_final"]] for c in paes.plan_chunks(e["total"], e["workers"])]
+        assert got == e["chunks"], (e["total"], e["workers"])
+    with pytest.raises(ValueError):
+        paes.plan_chunks(100, 0)
+
+
+def test_plan_grid_vs_oracle(paes, orc):
+    for total in range(0, 513, 5):
+        for w in range(1, 18):
+            got = [(c["offset"], c["raw_len"], c["padded_len"], c["is_final"]) for c in paes.plan_chunks(total, w)]
+            assert got == orc.plan(0, total, w)
+            if total and total % 16 == 0:
+                got = [(c["offset"], c["raw_len"], c["padded_len"], c["is_final"])
+                       for c in paes.plan_decrypt_chunks(total, w)]
+                assert got == orc.plan(1, total, w)
+
+
+def test_plan_decrypt_errors(paes):
+    """test_chunk.cpp:165-176."""
+    p = paes.plan_decrypt_chunks(1008, 4)
+    assert [c["raw_len"] for c in p] == [256, 256, 256, 240] and p[-1]["is_final"]
+    with pytest.raises(paes.PaddingError):
+        paes.plan_decrypt_chunks(0, 2)
+    with pytest.raises(paes.PaddingError):
+        paes.plan_decrypt_chunks(100, 2)
+    with pytest.raises(ValueError):
+        paes.plan_decrypt_chunks(1008, 0)
+
+
+def test_shards_cover_64gib_at_1_2_4_8(paes):
+    """The multi-GPU sharder on the config-4 size: contiguous, 16-B aligned, pad on the last."""
+    total = 64 << 30
+    for n in (1, 2, 4, 8):
+        p = paes.plan_chunks(total, n)
+        assert len(p) == n
+        off = 0
+        for i, c in enumerate(p):
+            assert c["offset"] == off and c["raw_len"] % 16 == 0
+            off += c["raw_len"]
+            assert c["is_final"] == (i == n - 1)
+        assert off == total and p[-1]["padded_len"] == p[-1]["raw_len"] + 16
+
+
+def test_pad_unpad(paes, golden):
+    """test_chunk.cpp:128-163 + golden."""
+    assert paes.pkcs7_pad(b"") == b"\x10" * 16
+    assert paes.pkcs7_unpad(paes.pkcs7_pad(b"abc")) == b"abc"
+    for e in golden["pad"]:
+        assert paes.pkcs7_pad(bytes.fromhex(e["in"])).hex() == e["out"]
+    for e in golden["unpad"]:
+        data = bytes.fromhex(e["in"])
+        if e["ok"]:
+            assert paes.pkcs7_unpad(data).hex() == e["out"]
+        else:
+            with pytest.raises(ValueError):
+                paes.pkcs7_unpad(data)
+    for n in range(0, 65):
+        data = bytes((i * 7 + 1) & 0xFF for i in range(n))
+        assert paes.pkcs7_unpad(paes.pkcs7_pad(data)) == data
+
+
+def test_reject_outliers_golden(paes, golden):
+    for e in golden["reject_outliers"]:
+        assert paes.reject_outliers(e["in"]) == pytest.approx(e["out"])
+    with pytest.raises(ValueError):
+        paes.reject_outliers([])
+
+
+def test_sweep_generator_matches_oracle(paes, orc):
+    assert paes.sweep(0, 16).hex() == "4c287f4282c15e6cfda0c041590ebc2a"
+    for seed, n in [(0, 0), (1, 7), (2, 1031), (3, 16), ((4 << 32) + 9, 4096), (123, 100_001)]:
+        assert paes.sweep(seed, n) == orc.sweep(seed, n)
+
+
+def test_batch_lengths_and_counter_stream(paes, orc):
+    lens = paes.batch_lengths(4, 4096)
+    assert lens == orc.batch_lengths(4, 4096)
+    assert all(4096 <= L <= 4 << 20 and L % 16 == 0 for L in lens)
+    assert 1.8 * (1 << 30) < sum(lens) < 2.8 * (1 << 30)  # ~2.31 GiB expected
+    for off, n in [(0, 64), (8, 40), (4096, 1000), ((64 << 30) - 64, 64)]:
+        assert paes.counter_fill(3, off, n) == orc.counter_fill(3, off, n)
+    data = paes.counter_fill(3, 0, 1 << 16)
+    assert paes.checksum(data, 0) == orc.checksum(data, 0)
+    # additivity: shard checksums sum to the whole
+    a, b = data[: 1 << 15], data[1 << 15:]
+    assert (paes.checksum(a, 0) + paes.checksum(b, (1 << 15) // 8)) % (1 << 64) == paes.checksum(data, 0)
+
+
+def test_compute_without_gpu_fails_loudly(paes):
+    if paes.device_count() > 0:
+        pytest.skip("a GPU is visible")
+    with pytest.raises(paes.GpuError):
+        paes.encrypt_bytes(b"abc", bytes(16))
+    with pytest.raises(paes.GpuError):
+        paes.ecb_device(0, 0x1000, 0x1000, 16, paes.round_keys(bytes(16)))
+
+
+def test_argument_errors_before_device(paes):
+    with pytest.raises(ValueError):
+        paes.encrypt_ecb(bytes(15), bytes(16))
+    with pytest.raises(ValueError):
+        paes.encrypt_chunk(bytes(17), False, bytes(16))
+    with pytest.raises(paes.PaddingError):
+        paes.decrypt_bytes(b"", bytes(16))
+    with pytest.raises(ValueError):
+        paes.encrypt_file("/nonexistent", "/tmp/x", bytes(16), strategy="threads")
+    from paper_1403_7295_b200 import _native as N
+
+    L = N.load()
+    assert L.paes_cuda_ecb(7, None, None, 0, paes.round_keys(bytes(16)), 0) == N.EINVAL
+    assert L.paes_cuda_set_pipeline(15, 0) == N.EINVAL
+    assert b"multiple of 16" in L.paes_cuda_last_error()
+
+
+def test_missing_library_raises(tmp_path, monkeypatch):
+    from paper_1403_7295_b200 import _native
+
+    monkeypatch.setattr(_native, "_lib", None)
+    monkeypatch.setattr(_native, "lib_path", lambda: str(tmp_path / "nope.so"))
+    with pytest.raises(_native.NativeLibraryMissing):
+        _native.load()
