@@ -1,0 +1,217 @@
+// paes_gpu.hpp -- C++20 face of libpaes_cuda.so with the reference library's
+// signatures (header-only, over the C ABI in paes_cuda.h).
+//
+// A caller of the reference's proj/include/paes/{aes,chunk,exec,errors}.hpp
+// swaps `paes::` for `paes::gpu::` (or adds ExecStrategy::Gpu to run_job, see
+// INTEGRATION.md) and gets the same bytes back from the sm_100a kernels:
+//
+//   reference (proj/include/paes/...)            here
+//   aes::Key128, aes::RoundKeySchedule          gpu::Key128, gpu::RoundKeySchedule   (aes.hpp:19-50)
+//   aes::encrypt_ecb / decrypt_ecb              gpu::encrypt_ecb / decrypt_ecb       (aes.hpp:86-89)
+//   aes::encrypt_block / decrypt_block          gpu::encrypt_block / decrypt_block   (aes.hpp:81-82)
+//   encrypt_chunk / decrypt_chunk               gpu::encrypt_chunk / decrypt_chunk   (exec.hpp:61-65)
+//   plan_chunks / plan_decrypt_chunks           gpu::plan_chunks / ...               (chunk.hpp:37-47)
+//   pad_final / unpad_final                     gpu::pad_final / unpad_final         (chunk.hpp:49-54)
+//   run_job(JobSpec) + ExecStrategy             gpu::run_job (strategy "gpu")        (exec.hpp:18-51)
+//   Error / IoError / PaddingError / WorkerError  same names, same bases           (errors.hpp:8-33)
+//
+// Error codes from the C ABI are rethrown as the reference's exception types.
+#pragma once
+
+#include <array>
+#include <cstdint>
+#include <filesystem>
+#include <span>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "paes_cuda.h"
+
+namespace paes::gpu {
+
+// ---- errors (errors.hpp:8-33) ---------------------------------------------
+class Error : public std::runtime_error {
+ public:
+  using std::runtime_error::runtime_error;
+};
+class IoError : public Error {
+ public:
+  explicit IoError(const std::string& what) : Error(what) {}
+};
+class PaddingError : public Error {
+ public:
+  using Error::Error;
+};
+class WorkerError : public Error {
+ public:
+  using Error::Error;
+};
+
+inline void check(long long rc) {
+  if (rc >= 0) return;
+  const std::string msg = paes_cuda_last_error();
+  switch (rc) {
+    case PAES_EINVAL: throw std::invalid_argument(msg);
+    case PAES_EBADMSG: throw PaddingError(msg);
+    case PAES_EIO: throw IoError(msg);
+    case PAES_EWORKER: throw WorkerError(msg);
+    default: throw Error(msg + " (paes_cuda code " + std::to_string(rc) + ")");
+  }
+}
+
+// ---- keys (aes.hpp:13-50) ---------------------------------------------------
+inline constexpr std::size_t kBlockSize = 16;
+inline constexpr int kRounds = 10;
+using Block = std::array<std::uint8_t, kBlockSize>;
+using RoundKey = std::array<std::uint8_t, kBlockSize>;
+
+struct Key128 {
+  std::array<std::uint8_t, kBlockSize> bytes{};
+  friend bool operator==(const Key128&, const Key128&) = default;
+};
+
+// Expanded on the host (north_star (1)); immutable, shareable across threads.
+class RoundKeySchedule {
+ public:
+  explicit RoundKeySchedule(const Key128& key) { check(paes_cuda_expand_key(key.bytes.data(), rk_.data())); }
+  RoundKey round_key(int round) const {
+    RoundKey k{};
+    for (std::size_t i = 0; i < kBlockSize; ++i) k[i] = rk_[16 * static_cast<std::size_t>(round) + i];
+    return k;
+  }
+  static constexpr int size() { return kRounds + 1; }
+  const std::uint8_t* data() const { return rk_.data(); }
+
+ private:
+  std::array<std::uint8_t, 176> rk_{};
+};
+
+inline RoundKeySchedule expand_key(const Key128& key) { return RoundKeySchedule(key); }
+
+// ---- bulk ECB (aes.hpp:84-89): len % 16 == 0, in/out same length, may alias
+inline void encrypt_ecb(std::span<const std::uint8_t> in, std::span<std::uint8_t> out, const RoundKeySchedule& ks,
+                        int ngpus = 0) {
+  if (in.size() != out.size() || in.size() % kBlockSize != 0)
+    throw std::invalid_argument("encrypt_ecb: length must be a multiple of 16 and match output");
+  check(paes_cuda_ecb(PAES_ENCRYPT, in.data(), out.data(), in.size(), ks.data(), ngpus));
+}
+
+inline void decrypt_ecb(std::span<const std::uint8_t> in, std::span<std::uint8_t> out, const RoundKeySchedule& ks,
+                        int ngpus = 0) {
+  if (in.size() != out.size() || in.size() % kBlockSize != 0)
+    throw std::invalid_argument("decrypt_ecb: length must be a multiple of 16 and match output");
+  check(paes_cuda_ecb(PAES_DECRYPT, in.data(), out.data(), in.size(), ks.data(), ngpus));
+}
+
+inline Block encrypt_block(const Block& in, const RoundKeySchedule& ks) {
+  Block out{};
+  encrypt_ecb(in, out, ks, 1);
+  return out;
+}
+
+inline Block decrypt_block(const Block& in, const RoundKeySchedule& ks) {
+  Block out{};
+  decrypt_ecb(in, out, ks, 1);
+  return out;
+}
+
+// ---- chunk transforms (exec.hpp:61-65) --------------------------------------
+inline std::vector<std::uint8_t> encrypt_chunk(std::span<const std::uint8_t> raw, bool is_final,
+                                               const RoundKeySchedule& ks, int ngpus = 0) {
+  if (!is_final && raw.size() % kBlockSize != 0)
+    throw std::invalid_argument("non-final chunk length must be a multiple of 16");
+  std::vector<std::uint8_t> out(is_final ? (raw.size() / kBlockSize + 1) * kBlockSize : raw.size());
+  std::uint64_t n = 0;
+  check(paes_cuda_chunk(PAES_ENCRYPT, raw.data(), raw.size(), is_final ? 1 : 0, ks.data(), out.data(), &n, ngpus));
+  out.resize(n);
+  return out;
+}
+
+inline std::vector<std::uint8_t> decrypt_chunk(std::span<const std::uint8_t> cipher, bool is_final,
+                                               const RoundKeySchedule& ks, int ngpus = 0) {
+  std::vector<std::uint8_t> out(cipher.size());
+  std::uint64_t n = 0;
+  check(paes_cuda_chunk(PAES_DECRYPT, cipher.data(), cipher.size(), is_final ? 1 : 0, ks.data(), out.data(), &n,
+                        ngpus));
+  out.resize(n);
+  return out;
+}
+
+// ---- chunk planner (chunk.hpp:18-59) ----------------------------------------
+inline constexpr std::uint64_t kBlock = 16;
+
+struct ChunkSpec {
+  std::uint64_t offset = 0, raw_len = 0, padded_len = 0;
+  bool is_final = false;
+  friend bool operator==(const ChunkSpec&, const ChunkSpec&) = default;
+};
+
+struct ChunkPlan {
+  std::uint64_t total_len = 0;
+  unsigned workers = 1;
+  std::vector<ChunkSpec> chunks;
+  std::uint64_t output_len() const {
+    std::uint64_t s = 0;
+    for (const auto& c : chunks) s += c.padded_len;
+    return s;
+  }
+};
+
+namespace detail {
+template <class F>
+ChunkPlan plan_with(F fn, std::uint64_t len, unsigned workers) {
+  const std::int64_t n = fn(len, workers, nullptr, 0);
+  check(n);
+  std::vector<paes_chunk_spec> specs(static_cast<std::size_t>(n));
+  check(fn(len, workers, specs.data(), specs.size()));
+  ChunkPlan p{len, workers, {}};
+  for (const auto& s : specs) p.chunks.push_back({s.offset, s.raw_len, s.padded_len, s.is_final != 0});
+  return p;
+}
+}  // namespace detail
+
+inline ChunkPlan plan_chunks(std::uint64_t total_len, unsigned workers) {
+  return detail::plan_with(paes_cuda_plan_chunks, total_len, workers);
+}
+inline ChunkPlan plan_decrypt_chunks(std::uint64_t cipher_len, unsigned workers) {
+  return detail::plan_with(paes_cuda_plan_decrypt_chunks, cipher_len, workers);
+}
+
+inline std::vector<std::uint8_t> pad_final(std::span<const std::uint8_t> raw) {
+  std::vector<std::uint8_t> out((raw.size() / kBlock + 1) * kBlock);
+  check(paes_cuda_pad_final(raw.data(), raw.size(), out.data()));
+  return out;
+}
+
+inline std::size_t unpad_final(std::span<const std::uint8_t> padded) {
+  const std::int64_t n = paes_cuda_unpad_final(padded.data(), padded.size());
+  check(n);
+  return static_cast<std::size_t>(n);
+}
+
+// ---- run_job with the GPU strategy (exec.hpp:18-51, exec.cpp:340-347) ------
+enum class Direction { Encrypt, Decrypt };
+
+struct JobSpec {
+  std::filesystem::path input_path;
+  std::filesystem::path output_path;
+  Key128 key;
+  unsigned workers = 1;  // GPUs; 0 = all visible
+  Direction direction = Direction::Encrypt;
+};
+
+struct JobOutcome {
+  std::uint64_t bytes_in = 0;
+  std::uint64_t bytes_out = 0;
+  double seconds = 0.0;
+};
+
+inline JobOutcome run_job(const JobSpec& job) {
+  paes_job_outcome o{};
+  check(paes_cuda_run_job(job.input_path.c_str(), job.output_path.c_str(), job.key.bytes.data(), job.workers,
+                          job.direction == Direction::Encrypt ? PAES_ENCRYPT : PAES_DECRYPT, &o));
+  return {o.bytes_in, o.bytes_out, o.seconds};
+}
+
+}  // namespace paes::gpu

@@ -1,0 +1,175 @@
+// C++ tests of include/paes_gpu.hpp (the reference-signature shim over the
+// C ABI), mirroring the reference's doctest cases.  Built and run by
+// tests/test_cpp_shim.py:   test_shim host   (no GPU: planner, pad, keys, errors)
+//                           test_shim gpu    (B200: ECB / chunk / run_job)
+#include <unistd.h>
+
+#include <cstdio>
+#include <cstdlib>
+#include <filesystem>
+#include <fstream>
+#include <random>
+#include <string>
+#include <vector>
+
+#include "paes_gpu.hpp"
+
+namespace gpu = paes::gpu;
+
+static int g_fail = 0;
+#define CHECK(c)                                                      \
+  do {                                                                \
+    if (!(c)) {                                                       \
+      std::fprintf(stderr, "%s:%d CHECK failed: %s\n", __FILE__, __LINE__, #c); \
+      ++g_fail;                                                       \
+    }                                                                 \
+  } while (0)
+
+template <class E, class F>
+static bool throws(F&& f) {
+  try {
+    f();
+  } catch (const E&) {
+    return true;
+  } catch (...) {
+    return false;
+  }
+  return false;
+}
+
+static std::vector<std::uint8_t> hex(const std::string& h) {
+  std::vector<std::uint8_t> v;
+  for (std::size_t i = 0; i + 1 < h.size(); i += 2) v.push_back(static_cast<std::uint8_t>(std::stoi(h.substr(i, 2), nullptr, 16)));
+  return v;
+}
+
+static gpu::Key128 key_hex(const std::string& h) {
+  gpu::Key128 k;
+  const auto v = hex(h);
+  std::copy(v.begin(), v.end(), k.bytes.begin());
+  return k;
+}
+
+static void host_tests() {
+  // key schedule KATs (test_aes.cpp:107-134)
+  const gpu::RoundKeySchedule zero(gpu::Key128{});
+  CHECK(zero.round_key(0) == gpu::RoundKey{});
+  const auto r1 = zero.round_key(1);
+  CHECK(std::vector<std::uint8_t>(r1.begin(), r1.end()) == hex("62636363626363636263636362636363"));
+  const gpu::RoundKeySchedule fips(key_hex("2b7e151628aed2a6abf7158809cf4f3c"));
+  CHECK(fips.round_key(1)[0] == 0xa0 && fips.round_key(1)[1] == 0xfa && fips.round_key(1)[2] == 0xfe &&
+        fips.round_key(1)[3] == 0x17);
+  // planner (test_chunk.cpp:57-117)
+  auto p = gpu::plan_chunks(1000, 4);
+  CHECK(p.chunks.size() == 4 && p.chunks[3].raw_len == 232 && p.chunks[3].padded_len == 240);
+  CHECK(gpu::plan_chunks(16, 1).chunks[0].padded_len == 32);
+  CHECK(gpu::plan_chunks(0, 33).chunks.size() == 1 && gpu::plan_chunks(0, 33).chunks[0].padded_len == 16);
+  CHECK(gpu::plan_chunks(17, 33).chunks.size() == 2);
+  CHECK(throws<std::invalid_argument>([] { gpu::plan_chunks(100, 0); }));
+  for (std::uint64_t total : {0ull, 1ull, 15ull, 16ull, 17ull, 1000ull, 1024ull})
+    for (unsigned w : {1u, 2u, 5u, 32u}) CHECK(gpu::plan_chunks(total, w).output_len() == (total / 16 + 1) * 16);
+  auto d = gpu::plan_decrypt_chunks(1008, 4);
+  CHECK(d.chunks.size() == 4 && d.chunks[0].raw_len == 256 && d.chunks[3].raw_len == 240 && d.chunks[3].is_final);
+  CHECK(throws<gpu::PaddingError>([] { gpu::plan_decrypt_chunks(0, 2); }));
+  CHECK(throws<gpu::PaddingError>([] { gpu::plan_decrypt_chunks(100, 2); }));
+  CHECK(throws<std::invalid_argument>([] { gpu::plan_decrypt_chunks(1008, 0); }));
+  // pad / unpad (test_chunk.cpp:128-163)
+  CHECK(gpu::pad_final({}) == std::vector<std::uint8_t>(16, 0x10));
+  std::vector<std::uint8_t> fifteen(15, 0xaa);
+  CHECK(gpu::pad_final(fifteen).back() == 0x01);
+  for (std::size_t len = 0; len <= 64; ++len) {
+    std::vector<std::uint8_t> data(len);
+    for (std::size_t i = 0; i < len; ++i) data[i] = static_cast<std::uint8_t>(i * 7 + 1);
+    CHECK(gpu::unpad_final(gpu::pad_final(data)) == len);
+  }
+  CHECK(throws<gpu::PaddingError>([] { gpu::unpad_final({}); }));
+  CHECK(throws<gpu::PaddingError>([] { gpu::unpad_final(std::vector<std::uint8_t>(16, 0x00)); }));
+  CHECK(throws<gpu::PaddingError>([] { gpu::unpad_final(std::vector<std::uint8_t>(16, 0x11)); }));
+  std::vector<std::uint8_t> inconsistent(16, 0x04);
+  inconsistent[13] = 0x05;
+  CHECK(throws<gpu::PaddingError>([&] { gpu::unpad_final(inconsistent); }));
+  // argument errors before any device work
+  std::vector<std::uint8_t> fifteen_b(15), out(15);
+  CHECK(throws<std::invalid_argument>([&] { gpu::encrypt_ecb(fifteen_b, out, zero); }));
+  CHECK(throws<std::invalid_argument>([&] { gpu::encrypt_chunk(std::vector<std::uint8_t>(17), false, zero); }));
+}
+
+static void gpu_tests() {
+  // FIPS-197 (test_aes.cpp:255-269)
+  const gpu::RoundKeySchedule ks(key_hex("000102030405060708090a0b0c0d0e0f"));
+  gpu::Block pt{};
+  const auto pv = hex("00112233445566778899aabbccddeeff");
+  std::copy(pv.begin(), pv.end(), pt.begin());
+  const auto ct = gpu::encrypt_block(pt, ks);
+  CHECK(std::vector<std::uint8_t>(ct.begin(), ct.end()) == hex("69c4e0d86a7b0430d8cdb78070b4c55a"));
+  CHECK(gpu::decrypt_block(ct, ks) == pt);
+  // zero-key snapshot (test_aes.cpp:285-292)
+  const auto snap = gpu::decrypt_block(gpu::Block{}, gpu::RoundKeySchedule(gpu::Key128{}));
+  CHECK(std::vector<std::uint8_t>(snap.begin(), snap.end()) == hex("140f0f1011b5223d79587717ffd9ec3a"));
+  // ECB property (test_aes.cpp:294-312)
+  std::vector<std::uint8_t> zeros(256, 0), enc(256), back(256);
+  gpu::encrypt_ecb(zeros, enc, ks);
+  const auto one = gpu::encrypt_block(gpu::Block{}, ks);
+  for (int b = 0; b < 16; ++b) CHECK(std::equal(one.begin(), one.end(), enc.begin() + 16 * b));
+  gpu::decrypt_ecb(enc, back, ks);
+  CHECK(back == zeros);
+  // chunk round trips across ragged sizes (test_exec.cpp:64-86, 139-155)
+  std::mt19937_64 rng(101);
+  for (std::size_t n : {0ul, 1ul, 15ul, 16ul, 17ul, 31ul, 32ul, 1000ul, 65536ul, 1ul << 20}) {
+    std::vector<std::uint8_t> data(n);
+    for (auto& x : data) x = static_cast<std::uint8_t>(rng());
+    const auto c = gpu::encrypt_chunk(data, true, ks);
+    CHECK(c.size() == (n / 16 + 1) * 16);
+    CHECK(gpu::decrypt_chunk(c, true, ks) == data);
+    // region independence (test_exec.cpp:291-312): two chunks == one final chunk
+    if (n >= 32 && n % 16 == 0) {
+      const auto first = gpu::encrypt_chunk(std::span(data).subspan(0, 16), false, ks);
+      const auto rest = gpu::encrypt_chunk(std::span(data).subspan(16), true, ks);
+      CHECK(std::equal(first.begin(), first.end(), c.begin()));
+      CHECK(std::equal(rest.begin(), rest.end(), c.begin() + 16));
+    }
+  }
+  // wrong key -> PaddingError (test_exec.cpp:235-247)
+  std::vector<std::uint8_t> msg(100, 7);
+  const auto c = gpu::encrypt_chunk(msg, true, ks);
+  gpu::Key128 bad = key_hex("000102030405060708090a0b0c0d0e0f");
+  bad.bytes[0] ^= 0xff;
+  CHECK(throws<gpu::PaddingError>([&] { gpu::decrypt_chunk(c, true, gpu::RoundKeySchedule(bad)); }));
+  // run_job (test_exec.cpp:139-155, 249-267) with the gpu strategy
+  const auto dir = std::filesystem::temp_directory_path() / ("paes_shim_" + std::to_string(::getpid()));
+  std::filesystem::create_directories(dir);
+  std::vector<std::uint8_t> big(1 << 20);
+  for (auto& x : big) x = static_cast<std::uint8_t>(rng());
+  {
+    std::ofstream f(dir / "mb.bin", std::ios::binary);
+    f.write(reinterpret_cast<const char*>(big.data()), static_cast<std::streamsize>(big.size()));
+  }
+  gpu::JobSpec job{dir / "mb.bin", dir / "mb.enc", key_hex("000102030405060708090a0b0c0d0e0f"), 1,
+                   gpu::Direction::Encrypt};
+  const auto o = gpu::run_job(job);
+  CHECK(o.bytes_in == (1u << 20) && o.bytes_out == (1u << 20) + 16);
+  gpu::JobSpec dec{dir / "mb.enc", dir / "mb.dec", job.key, 1, gpu::Direction::Decrypt};
+  CHECK(gpu::run_job(dec).bytes_out == (1u << 20));
+  std::ifstream in(dir / "mb.dec", std::ios::binary);
+  std::vector<std::uint8_t> got((std::istreambuf_iterator<char>(in)), std::istreambuf_iterator<char>());
+  CHECK(got == big);
+  gpu::JobSpec wrong = dec;
+  wrong.output_path = dir / "bad.dec";
+  wrong.key.bytes[5] ^= 0x01;
+  try {
+    gpu::run_job(wrong);
+    CHECK(false);
+  } catch (const gpu::WorkerError& e) {
+    CHECK(std::string(e.what()).find("chunk 0") != std::string::npos);
+  }
+  CHECK(!std::filesystem::exists(dir / "bad.dec"));
+  std::filesystem::remove_all(dir);
+}
+
+int main(int argc, char** argv) {
+  const std::string mode = argc > 1 ? argv[1] : "host";
+  host_tests();
+  if (mode == "gpu") gpu_tests();
+  std::printf("%s: %s (%d failures)\n", mode.c_str(), g_fail ? "FAIL" : "ok", g_fail);
+  return g_fail ? 1 : 0;
+}

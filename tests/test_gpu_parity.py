@@ -325,7 +325,7 @@ def test_config4_64gib_device_generated(paes, gpu, digests):
     free, _ = torch.cuda.mem_get_info()
     if free < 2 * total + GiB:
         pytest.fail(f"config 4 needs {2 * total + GiB} bytes of HBM, {free} free")
-    pt = torch.empty(total, dtype=torch.uint8, device="cuda")
+    pt = torch.empty(total + 16, dtype=torch.uint8, device="cuda")  # decrypt writes len bytes back
     ct = torch.empty(total + 16, dtype=torch.uint8, device="cuda")
     paes.counter_fill_device(3, 0, total, pt.data_ptr())
     assert paes.checksum_device(pt.data_ptr(), total, 0) == d["pt_checksum"]
