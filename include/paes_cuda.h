@@ -70,7 +70,7 @@ int paes_cuda_device_count(void);
  * restores the default.  One process per GPU (torchrun) sets {local_rank}. */
 int paes_cuda_set_devices(const int* ids, int n);
 /* Host-pointer pipeline tuning: staging chunk (bytes, multiple of 16) and
- * streams per device (>= 1).  0 keeps the current value.  Defaults 32 MiB, 4. */
+ * streams per device (>= 1).  0 keeps the current value.  Defaults 64 MiB, 3. */
 int paes_cuda_set_pipeline(uint64_t chunk_bytes, int streams);
 
 /* ---- host-side rules (no GPU needed) ------------------------------------ */

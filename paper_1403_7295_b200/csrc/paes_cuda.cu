@@ -104,8 +104,8 @@ constexpr int kMaxDev = 64;
 DevCtx g_dev[kMaxDev];
 std::mutex g_cfg_mu;
 std::vector<int> g_devices;  // empty = all visible
-std::uint64_t g_chunk = 32ull << 20;
-int g_streams = 4;
+std::uint64_t g_chunk = 64ull << 20;  // scripts/pcie_probe.py: 64-128 MiB pieces reach ~94% of concurrent H2D+D2H
+int g_streams = 3;
 
 int visible_devices() {
   int n = 0;

@@ -127,7 +127,7 @@ def test_pipeline_piece_boundaries(paes, gpu, orc):
             assert ct == orc.encrypt_chunk(data, True, key), n
             assert paes.decrypt_bytes(ct, key) == data
     finally:
-        paes.set_pipeline(32 * MiB, 4)
+        paes.set_pipeline(64 * MiB, 3)
 
 
 def test_in_place_host(paes, gpu, orc):
@@ -246,7 +246,7 @@ def test_file_pipeline_many_pieces(paes, gpu, orc, tmp_path):
         paes.decrypt_file(str(tmp_path / "b"), str(tmp_path / "c"), key)
         assert (tmp_path / "c").read_bytes() == data
     finally:
-        paes.set_pipeline(32 * MiB, 4)
+        paes.set_pipeline(64 * MiB, 3)
 
 
 # ------------------------------------------------------------ BASELINE.json configs
