@@ -134,6 +134,17 @@ int paes_cuda_ecb_batch(int dir, const void* d_in, void* d_out, const uint64_t* 
                         const uint64_t* lens, const uint8_t* rks, uint32_t n, int pad, uint64_t* out_lens,
                         int device, void* stream);
 
+/* Prepared batch: the per-message descriptor table and kernel key words are
+ * built and uploaded once (the RoundKeySchedule-per-job pattern of
+ * exec.cpp:148, 368); each run is then one launch over any buffers with that
+ * layout.  Same semantics as paes_cuda_ecb_batch.  A plan may be run from one
+ * thread at a time. */
+typedef struct paes_batch_plan paes_batch_plan;
+int paes_cuda_batch_plan_create(int dir, const uint64_t* in_off, const uint64_t* out_off, const uint64_t* lens,
+                                const uint8_t* rks, uint32_t n, int pad, int device, paes_batch_plan** plan);
+int paes_cuda_batch_plan_run(paes_batch_plan* plan, const void* d_in, void* d_out, uint64_t* out_lens, void* stream);
+void paes_cuda_batch_plan_destroy(paes_batch_plan* plan);
+
 /* ---- file path: ExecStrategy "gpu" for run_job (exec.hpp:18-45) ---------
  * File -> file through pinned ring buffers (pread -> H2D -> kernel -> D2H ->
  * pwrite), output written under a temporary name and renamed on success

@@ -59,6 +59,10 @@ SIGNATURES = [
     ("paes_cuda_chunk_device", C.c_int, [C.c_int, _vp, _u64, C.c_int, _vp, _vp, C.POINTER(_u64), C.c_int, _vp]),
     ("paes_cuda_ecb_batch", C.c_int, [C.c_int, _vp, _vp, C.POINTER(_u64), C.POINTER(_u64), C.POINTER(_u64), _vp,
                                       C.c_uint32, C.c_int, C.POINTER(_u64), C.c_int, _vp]),
+    ("paes_cuda_batch_plan_create", C.c_int, [C.c_int, C.POINTER(_u64), C.POINTER(_u64), C.POINTER(_u64), _vp,
+                                              C.c_uint32, C.c_int, C.c_int, C.POINTER(_vp)]),
+    ("paes_cuda_batch_plan_run", C.c_int, [_vp, _vp, _vp, C.POINTER(_u64), _vp]),
+    ("paes_cuda_batch_plan_destroy", None, [_vp]),
     ("paes_cuda_run_job", C.c_int, [C.c_char_p, C.c_char_p, _vp, C.c_uint32, C.c_int, C.POINTER(JobOutcome)]),
     ("paes_cuda_sweep", C.c_int, [_u64, _u64, _vp]),
     ("paes_cuda_batch_lengths", C.c_int, [_u64, C.c_uint32, C.POINTER(_u64)]),

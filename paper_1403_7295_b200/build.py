@@ -35,15 +35,20 @@ def _stale() -> bool:
     return any(os.path.getmtime(p) > t for p in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not _stale():
+def build(force: bool = False, verbose: bool = False, defines=(), out_lib: str | None = None) -> str:
+    """Compile + link.  `defines` (e.g. ["PAES_NB=4"]) and `out_lib` are for
+    tuning variants (scripts/tune_variants.py); the product uses the defaults."""
+    lib = out_lib or LIB
+    if not force and out_lib is None and not _stale():
         return LIB
-    os.makedirs(LIB_DIR, exist_ok=True)
+    lib_dir = os.path.dirname(lib)
+    os.makedirs(lib_dir, exist_ok=True)
+    dflags = ["-D" + d for d in defines]
     from concurrent.futures import ThreadPoolExecutor
 
     def compile_one(src):
-        obj = os.path.join(LIB_DIR, src + ".o")
-        cmd = [NVCC] + CCBIN + ARCH + FLAGS + ["-c", os.path.join(CSRC, src), "-o", obj]
+        obj = os.path.join(lib_dir, src + ".o")
+        cmd = [NVCC] + CCBIN + ARCH + FLAGS + dflags + ["-c", os.path.join(CSRC, src), "-o", obj]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError("nvcc failed for %s:\n%s%s" % (src, r.stdout, r.stderr))
@@ -53,15 +58,15 @@ def build(force: bool = False, verbose: bool = False) -> str:
 
     with ThreadPoolExecutor(len(SOURCES)) as ex:
         objs = list(ex.map(compile_one, SOURCES))
-    tmp = LIB + ".tmp"
+    tmp = lib + ".tmp"
     cmd = [NVCC] + CCBIN + ARCH + ["-shared", "-o", tmp] + objs + ["-lpthread"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError("link failed:\n%s%s" % (r.stdout, r.stderr))
-    os.replace(tmp, LIB)
+    os.replace(tmp, lib)
     for o in objs:
         os.unlink(o)
-    return LIB
+    return lib
 
 
 if __name__ == "__main__":

@@ -17,7 +17,10 @@ std::atomic<unsigned long long> g_launches{0};
 
 namespace {
 
-constexpr int kThreads = 512;  // one persistent CTA per SM (smem-limited)
+#ifndef PAES_THREADS
+#define PAES_THREADS 512
+#endif
+constexpr int kThreads = PAES_THREADS;  // one persistent CTA per SM (smem-limited)
 
 // ---------------------------------------------------------------- staging
 // Replicate the tables 32x (one copy per bank) into the CTA's shared memory.
@@ -240,9 +243,10 @@ __global__ void __launch_bounds__(kThreads, 1) ecb_kernel(const __grid_constant_
 }
 
 // ---------------------------------------------------------------- batch
-// Persistent warps over a contiguous range of warp tiles of the concatenated
-// block stream; a warp's tiles advance monotonically through the messages,
-// so its key registers are reloaded only when it crosses a message.
+// Persistent warps over a contiguous range of warp tiles.  Each message owns
+// whole tiles (BatchMsg::first_tile), so a tile never mixes keys: a warp
+// reloads its 44 key registers only when it moves to the next message, and
+// the only per-block checks are on the message's ragged last tile.
 template <bool DEC, int NB>
 __global__ void __launch_bounds__(kThreads, 1) batch_kernel(const __grid_constant__ BatchArgs a) {
   extern __shared__ __align__(16) std::uint32_t sm[];
@@ -252,72 +256,78 @@ __global__ void __launch_bounds__(kThreads, 1) batch_kernel(const __grid_constan
   const std::uint32_t lane = threadIdx.x & 31;
   const std::uint32_t lane4 = lane * 4;
   constexpr unsigned long long kTile = 32ull * NB;
-  const unsigned long long ntiles = (a.total_blocks + kTile - 1) / kTile;
   const unsigned long long nwarps = static_cast<unsigned long long>(gridDim.x) * (blockDim.x / 32);
   const unsigned long long warp = static_cast<unsigned long long>(blockIdx.x) * (blockDim.x / 32) + threadIdx.x / 32;
-  const unsigned long long t_begin = ntiles * warp / nwarps;
-  const unsigned long long t_end = ntiles * (warp + 1) / nwarps;
+  const unsigned long long t_begin = a.total_tiles * warp / nwarps;
+  const unsigned long long t_end = a.total_tiles * (warp + 1) / nwarps;
   if (t_begin >= t_end) return;
 
-  // message holding the warp's first block (binary search, warp-uniform)
+  // last message whose first tile is <= t_begin (binary search, warp-uniform)
   std::uint32_t m = 0;
   {
-    const unsigned long long g0 = t_begin * kTile;
-    std::uint32_t lo = 0, hi = a.nmsg;  // last msg with first <= g0
+    std::uint32_t lo = 0, hi = a.nmsg;
     while (hi - lo > 1) {
       const std::uint32_t mid = (lo + hi) / 2;
-      if (a.msgs[mid].first <= g0) lo = mid;
+      if (a.msgs[mid].first_tile <= t_begin) lo = mid;
       else hi = mid;
     }
     m = lo;
   }
+  // the current message's descriptor, keys and the next message's first tile
+  // stay in registers: no global traffic per tile except at message changes
   std::uint32_t kw[44];
-  std::uint32_t key_m = 0xffffffffu;
+  BatchMsg msg;
+  unsigned long long next_first = 0;
+  auto enter = [&](std::uint32_t mi) {
+    msg = a.msgs[mi];
+    next_first = mi + 1 < a.nmsg ? a.msgs[mi + 1].first_tile : ~0ull;
+    const uint4* kp = reinterpret_cast<const uint4*>(a.keys + 44ull * mi);
+#pragma unroll
+    for (int i = 0; i < 11; ++i) {
+      const uint4 v = __ldg(kp + i);
+      kw[4 * i] = v.x;
+      kw[4 * i + 1] = v.y;
+      kw[4 * i + 2] = v.z;
+      kw[4 * i + 3] = v.w;
+    }
+  };
+  enter(m);
   for (unsigned long long tile = t_begin; tile < t_end; ++tile) {
-    const unsigned long long g0 = tile * kTile;
-    const unsigned long long g_last = min(g0 + kTile, a.total_blocks) - 1;
-    while (m + 1 < a.nmsg && a.msgs[m + 1].first <= g0) ++m;
-    const BatchMsg msg = a.msgs[m];
-    if (g0 + kTile <= a.total_blocks && g_last + a.check_pad < msg.first + msg.nfull) {
-      // fast path: the whole tile is whole input blocks of message m
-      if (key_m != m) {
-        const uint4* kp = reinterpret_cast<const uint4*>(a.keys + 44ull * m);
+    if (tile >= next_first) {
+      do {
+        ++m;
+      } while (m + 1 < a.nmsg && a.msgs[m + 1].first_tile <= tile);
+      enter(m);
+    }
+    const unsigned long long t0 = (tile - msg.first_tile) * kTile;  // first block of the tile in the message
+    const std::uint8_t* src = a.in + msg.in_off;
+    std::uint8_t* dst = a.out + msg.out_off;
+    Block4 s[NB];
+    if (t0 + kTile + a.check_pad <= msg.nfull) {
+      // whole input blocks only: no per-block checks
+      const unsigned long long lb = t0 + lane;
 #pragma unroll
-        for (int i = 0; i < 11; ++i) {
-          const uint4 v = __ldg(kp + i);
-          kw[4 * i] = v.x;
-          kw[4 * i + 1] = v.y;
-          kw[4 * i + 2] = v.z;
-          kw[4 * i + 3] = v.w;
-        }
-        key_m = m;
-      }
-      const unsigned long long lb = g0 - msg.first + lane;
-      const std::uint8_t* src = a.in + msg.in_off + 16ull * lb;
-      std::uint8_t* dst = a.out + msg.out_off + 16ull * lb;
-      Block4 s[NB];
-#pragma unroll
-      for (int j = 0; j < NB; ++j) s[j] = load_block<true>(src + 512ull * j);
+      for (int j = 0; j < NB; ++j) s[j] = load_block<true>(src + 16ull * (lb + 32ull * j));
       cipher<DEC, NB>(s, kw, smb, lane4);
 #pragma unroll
-      for (int j = 0; j < NB; ++j) store_block<true>(dst + 512ull * j, s[j]);
+      for (int j = 0; j < NB; ++j) store_block<true>(dst + 16ull * (lb + 32ull * j), s[j]);
     } else {
-      // boundary tile: block by block, keys read from global per message
-#pragma unroll 1
+      // the message's last tile: partial blocks, pad block, trailer check
+#pragma unroll
       for (int j = 0; j < NB; ++j) {
-        const unsigned long long g = g0 + lane + 32ull * j;
-        if (g >= a.total_blocks) break;
-        std::uint32_t mm = m;
-        while (mm + 1 < a.nmsg && a.msgs[mm + 1].first <= g) ++mm;
-        const BatchMsg bm = a.msgs[mm];
-        const unsigned long long lb = g - bm.first;
-        Block4 s1[1];
-        if (lb < bm.nfull) s1[0] = load_block<true>(a.in + bm.in_off + 16ull * lb);
-        else s1[0] = pad_block(a.in + bm.in_off + 16ull * bm.nfull, bm.tail_len);
-        const std::uint32_t* gk = a.keys + 44ull * mm;
-        cipher<DEC, 1>(s1, gk, smb, lane4);
-        store_block<true>(a.out + bm.out_off + 16ull * lb, s1[0]);
-        if (DEC && a.check_pad && lb == bm.nblocks - 1) a.status[mm] = pad_check(s1[0]);
+        const unsigned long long lb = t0 + lane + 32ull * j;
+        if (lb < msg.nfull) s[j] = load_block<true>(src + 16ull * lb);
+        else if (lb < msg.nblocks) s[j] = pad_block(src + 16ull * msg.nfull, msg.tail_len);
+        else s[j] = Block4{0, 0, 0, 0};
+      }
+      cipher<DEC, NB>(s, kw, smb, lane4);
+#pragma unroll
+      for (int j = 0; j < NB; ++j) {
+        const unsigned long long lb = t0 + lane + 32ull * j;
+        if (lb < msg.nblocks) {
+          store_block<true>(dst + 16ull * lb, s[j]);
+          if (DEC && a.check_pad && lb == msg.nblocks - 1) a.status[m] = pad_check(s[j]);
+        }
       }
     }
   }
@@ -380,7 +390,10 @@ cudaError_t set_smem(KernelT k, int bytes) {
 }  // namespace
 
 // ---------------------------------------------------------------- launchers
-constexpr int kNB = 2;  // blocks per thread per warp tile
+#ifndef PAES_NB
+#define PAES_NB 2
+#endif
+constexpr int kNB = PAES_NB;  // blocks per thread per warp tile
 
 cudaError_t prepare_kernels() {
   cudaError_t e;
@@ -411,10 +424,12 @@ cudaError_t launch_ecb(bool dec, const EcbArgs& args, int sm_count, cudaStream_t
   return cudaGetLastError();
 }
 
+unsigned batch_tile_blocks() { return 32u * kNB; }
+
 cudaError_t launch_batch(bool dec, const BatchArgs& args, int sm_count, cudaStream_t stream) {
-  if (args.total_blocks == 0) return cudaSuccess;
-  const unsigned long long per_cta = static_cast<unsigned long long>(kThreads) * kNB;
-  unsigned long long grid = (args.total_blocks + per_cta - 1) / per_cta;
+  if (args.total_tiles == 0) return cudaSuccess;
+  const unsigned long long per_cta = kThreads / 32;  // warp tiles per CTA per wave
+  unsigned long long grid = (args.total_tiles + per_cta - 1) / per_cta;
   if (grid > static_cast<unsigned long long>(sm_count)) grid = sm_count;
   const int smem = dec ? kDecSmemBytes : kEncSmemBytes;
   if (dec) batch_kernel<true, kNB><<<static_cast<unsigned>(grid), kThreads, smem, stream>>>(args);

@@ -68,13 +68,16 @@ struct EcbArgs {
   KeyWords k;
 };
 
-// Batch (config 5): message descriptors, device-resident.
+// Batch (config 5): message descriptors, device-resident.  Every message owns
+// ceil(nblocks / kBatchTile) whole warp tiles, so no tile straddles two
+// messages (a warp's key registers are uniform for a tile) and the ragged
+// last tile of each message is masked.
 struct BatchMsg {
-  unsigned long long in_off;   // byte offset of the message in d_in
-  unsigned long long out_off;  // byte offset of its output in d_out
-  unsigned long long first;    // first global block index of the message
-  unsigned long long nfull;    // whole input blocks
-  std::uint32_t nblocks;       // output blocks (nfull or nfull+1)
+  unsigned long long in_off;      // byte offset of the message in d_in
+  unsigned long long out_off;     // byte offset of its output in d_out
+  unsigned long long first_tile;  // first warp tile of the message
+  unsigned long long nfull;       // whole input blocks
+  std::uint32_t nblocks;          // output blocks (nfull or nfull+1)
   std::uint32_t tail_len;
 };
 
@@ -84,9 +87,12 @@ struct BatchArgs {
   const BatchMsg* msgs;
   const std::uint32_t* keys;         // 44 words per message, in order of use
   std::uint32_t* status;             // decrypt+pad: one word per message
-  unsigned long long total_blocks;
+  unsigned long long total_tiles;
   std::uint32_t nmsg;
   std::uint32_t check_pad;
 };
+
+// Blocks per warp tile of the batch kernel (32 lanes x blocks per lane).
+unsigned batch_tile_blocks();
 
 }  // namespace paes_b200

@@ -223,13 +223,22 @@ EcbArgs make_args(const Range& r, const std::uint8_t* in, std::uint8_t* out, std
   return a;
 }
 
+// Piece size for a range: the staging chunk, but small enough that even a
+// short range is split into ~2 pieces per stream so copy-in, kernel and
+// copy-out still overlap (a single 64 MiB piece would serialise them).
+std::uint64_t piece_size(std::uint64_t len, std::uint64_t chunk, int streams) {
+  const std::uint64_t floor_piece = std::min<std::uint64_t>(4ull << 20, chunk);
+  const std::uint64_t p = (len / (2ull * static_cast<std::uint64_t>(streams)) + 15) & ~std::uint64_t(15);
+  return std::clamp(p, floor_piece, chunk);
+}
+
 // Host range on one device through the stream ring (d.mu held).  Returns the
 // number of output bytes (decrypt+check: unpadded).
 std::uint64_t run_host_range(DevCtx& d, const Range& r, const std::uint8_t* in, std::uint8_t* out, const KeyWords& kw) {
   DeviceGuard g(d.id);
   ensure_pipeline(d, false);
-  const std::uint64_t C = d.chunk;
   const int S = static_cast<int>(d.st.size());
+  const std::uint64_t C = piece_size(r.in_len, d.chunk, S);
   const std::uint64_t npieces = std::max<std::uint64_t>(1, (r.in_len + C - 1) / C);
   std::uint64_t out_total = 0;
   for (std::uint64_t k = 0; k < npieces; ++k) {
@@ -468,77 +477,224 @@ int paes_cuda_chunk_device(int dir, const void* d_in, uint64_t len, int is_final
   });
 }
 
+}  // extern "C"
+
+// ------------------------------------------------------------ batch (config 5)
+namespace {
+
+// Host image of a batch: BatchMsg[n] | KeyWords[n] (| status words when the
+// trailers are checked).  Validation mirrors encrypt_chunk / decrypt_chunk per
+// message (exec.cpp:375-392).
+struct BatchImage {
+  bool dec = false, check = false;
+  std::uint32_t n = 0;
+  unsigned long long total_tiles = 0;  // warp tiles (each message owns whole tiles)
+  std::size_t msg_bytes = 0, image_bytes = 0, status_off = 0, total_bytes = 0;
+  std::vector<std::uint64_t> lens;
+  std::vector<std::uint32_t> nblocks;
+};
+
+BatchImage plan_batch(int dir, const uint64_t* in_off, const uint64_t* out_off, const uint64_t* lens,
+                      const uint8_t* rks, uint32_t n, int pad) {
+  if (dir != PAES_ENCRYPT && dir != PAES_DECRYPT) throw std::invalid_argument("bad dir");
+  if (n && (!in_off || !out_off || !lens || !rks)) throw std::invalid_argument("null batch descriptor");
+  BatchImage b;
+  b.dec = dir == PAES_DECRYPT;
+  b.check = b.dec && pad;
+  b.n = n;
+  b.msg_bytes = sizeof(BatchMsg) * n;
+  b.image_bytes = b.msg_bytes + sizeof(KeyWords) * n;
+  b.status_off = (b.image_bytes + 255) & ~std::size_t(255);
+  b.total_bytes = b.status_off + (b.check ? 4ull * n : 0);
+  b.lens.assign(lens, lens + n);
+  b.nblocks.resize(n);
+  for (uint32_t i = 0; i < n; ++i) {
+    if (in_off[i] % 16 || out_off[i] % 16) throw std::invalid_argument("batch offsets must be multiples of 16");
+    if ((b.dec || !pad) && lens[i] % 16) throw std::invalid_argument("message length must be a multiple of 16");
+    if (b.check && lens[i] == 0) throw PaddingError("unpad: length must be a non-zero multiple of 16");
+    const unsigned long long nb = lens[i] / 16 + ((pad && !b.dec) ? 1 : 0);
+    if (nb > 0xffffffffull) throw std::invalid_argument("message too large for the batch path");
+    b.nblocks[i] = static_cast<std::uint32_t>(nb);
+    b.total_tiles += (nb + batch_tile_blocks() - 1) / batch_tile_blocks();
+  }
+  return b;
+}
+
+void write_batch_image(const BatchImage& b, const uint64_t* in_off, const uint64_t* out_off, const uint8_t* rks,
+                       std::uint8_t* dst) {
+  auto* msgs = reinterpret_cast<BatchMsg*>(dst);
+  auto* keys = reinterpret_cast<KeyWords*>(dst + b.msg_bytes);
+  unsigned long long tile = 0;
+  for (uint32_t i = 0; i < b.n; ++i) {
+    BatchMsg m{};
+    m.in_off = in_off[i];
+    m.out_off = out_off[i];
+    m.first_tile = tile;
+    m.nfull = b.lens[i] / 16;
+    m.tail_len = static_cast<std::uint32_t>(b.lens[i] % 16);
+    m.nblocks = b.nblocks[i];
+    tile += (m.nblocks + batch_tile_blocks() - 1) / batch_tile_blocks();
+    msgs[i] = m;
+    keys[i] = b.dec ? dec_key_words(rks + 176ull * i) : enc_key_words(rks + 176ull * i);
+  }
+}
+
+BatchArgs batch_args(const BatchImage& b, const void* d_in, void* d_out, std::uint8_t* dd) {
+  BatchArgs a{};
+  a.in = static_cast<const std::uint8_t*>(d_in);
+  a.out = static_cast<std::uint8_t*>(d_out);
+  a.msgs = reinterpret_cast<const BatchMsg*>(dd);
+  a.keys = reinterpret_cast<const std::uint32_t*>(dd + b.msg_bytes);
+  a.status = b.check ? reinterpret_cast<std::uint32_t*>(dd + b.status_off) : nullptr;
+  a.total_tiles = b.total_tiles;
+  a.nmsg = b.n;
+  a.check_pad = b.check ? 1u : 0u;
+  return a;
+}
+
+void finish_lengths(const BatchImage& b, const std::uint32_t* status, uint64_t* out_lens) {
+  if (!b.check) {
+    if (out_lens)
+      for (uint32_t i = 0; i < b.n; ++i) out_lens[i] = static_cast<uint64_t>(b.nblocks[i]) * 16;
+    return;
+  }
+  bool bad = false;
+  for (uint32_t i = 0; i < b.n; ++i) {
+    const bool ok = status[i] != 0xffffffffu;
+    bad |= !ok;
+    if (out_lens) out_lens[i] = ok ? b.lens[i] - status[i] : UINT64_MAX;
+  }
+  if (bad) throw PaddingError("unpad: invalid pad bytes in one or more messages");
+}
+
+// Per-thread pinned staging for one-shot batches: the descriptor upload is a
+// true async copy, and the buffer is reused once its previous copy is done.
+struct Staging {
+  std::uint8_t* p = nullptr;
+  std::size_t cap = 0;
+  int device = -1;
+  cudaEvent_t ev = nullptr;
+  ~Staging() {
+    if (p) cudaFreeHost(p);
+  }
+};
+thread_local Staging t_stage;
+
+std::uint8_t* staging(std::size_t bytes, int device) {
+  Staging& st = t_stage;
+  if (st.ev && st.device == device) PAES_CK(cudaEventSynchronize(st.ev));
+  if (st.device != device) {
+    if (st.ev) cudaEventDestroy(st.ev);
+    st.ev = nullptr;
+    st.device = device;
+  }
+  if (!st.ev) PAES_CK(cudaEventCreateWithFlags(&st.ev, cudaEventDisableTiming));
+  if (st.cap < bytes) {
+    if (st.p) PAES_CK(cudaFreeHost(st.p));
+    st.p = nullptr;
+    st.cap = 0;
+    PAES_CK(cudaMallocHost(&st.p, bytes));
+    st.cap = bytes;
+  }
+  return st.p;
+}
+
+}  // namespace
+
+struct paes_batch_plan {
+  int device = -1;
+  BatchImage img;
+  std::uint8_t* dd = nullptr;        // device image
+  std::uint32_t* h_status = nullptr;  // pinned
+};
+
+extern "C" {
+
 int paes_cuda_ecb_batch(int dir, const void* d_in, void* d_out, const uint64_t* in_off, const uint64_t* out_off,
                         const uint64_t* lens, const uint8_t* rks, uint32_t n, int pad, uint64_t* out_lens,
                         int device_id, void* stream) {
   return guarded([&] {
-    if (dir != PAES_ENCRYPT && dir != PAES_DECRYPT) throw std::invalid_argument("bad dir");
+    const BatchImage b = plan_batch(dir, in_off, out_off, lens, rks, n, pad);
     if (n == 0) return PAES_OK;
-    if (!in_off || !out_off || !lens || !rks) throw std::invalid_argument("null batch descriptor");
-    const bool dec = dir == PAES_DECRYPT;
-    std::vector<BatchMsg> msgs(n);
-    std::vector<KeyWords> keys(n);
-    unsigned long long g = 0;
-    for (uint32_t i = 0; i < n; ++i) {
-      if (in_off[i] % 16 || out_off[i] % 16) throw std::invalid_argument("batch offsets must be multiples of 16");
-      if ((dec || !pad) && lens[i] % 16) throw std::invalid_argument("message length must be a multiple of 16");
-      if (dec && pad && lens[i] == 0) throw PaddingError("unpad: length must be a non-zero multiple of 16");
-      BatchMsg& m = msgs[i];
-      m.in_off = in_off[i];
-      m.out_off = out_off[i];
-      m.first = g;
-      m.nfull = lens[i] / 16;
-      m.tail_len = static_cast<std::uint32_t>(lens[i] % 16);
-      const unsigned long long nb = m.nfull + ((pad && !dec) ? 1 : 0);
-      if (nb > 0xffffffffull) throw std::invalid_argument("message too large for the batch path");
-      m.nblocks = static_cast<std::uint32_t>(nb);
-      g += nb;
-      keys[i] = dec ? dec_key_words(rks + 176ull * i) : enc_key_words(rks + 176ull * i);
-    }
     if (!d_in || !d_out) throw std::invalid_argument("null device buffer");
     DevCtx& d = device(device_id);
     DeviceGuard dg(device_id);
     cudaStream_t s = static_cast<cudaStream_t>(stream);
-    const bool check = dec && pad;
-    // descriptors: one device allocation, freed stream-ordered
-    const std::size_t msg_bytes = sizeof(BatchMsg) * n, key_bytes = sizeof(KeyWords) * n;
-    const std::size_t status_off = (msg_bytes + key_bytes + 255) & ~std::size_t(255);
-    const std::size_t total = status_off + (check ? 4ull * n : 0);
-    std::vector<std::uint8_t> host(total, 0);
-    std::memcpy(host.data(), msgs.data(), msg_bytes);
-    std::memcpy(host.data() + msg_bytes, keys.data(), key_bytes);
+    std::uint8_t* host = staging(b.total_bytes, device_id);
+    write_batch_image(b, in_off, out_off, rks, host);
     std::uint8_t* dd = nullptr;
-    PAES_CK(cudaMallocAsync(reinterpret_cast<void**>(&dd), total, s));
-    PAES_CK(cudaMemcpyAsync(dd, host.data(), status_off, cudaMemcpyHostToDevice, s));
-    BatchArgs a{};
-    a.in = static_cast<const std::uint8_t*>(d_in);
-    a.out = static_cast<std::uint8_t*>(d_out);
-    a.msgs = reinterpret_cast<const BatchMsg*>(dd);
-    a.keys = reinterpret_cast<const std::uint32_t*>(dd + msg_bytes);
-    a.status = check ? reinterpret_cast<std::uint32_t*>(dd + status_off) : nullptr;
-    a.total_blocks = g;
-    a.nmsg = n;
-    a.check_pad = check ? 1u : 0u;
-    PAES_CK(launch_batch(dec, a, d.sm_count, s));
-    if (check) {
-      std::vector<std::uint32_t> st(n);
-      PAES_CK(cudaMemcpyAsync(st.data(), dd + status_off, 4ull * n, cudaMemcpyDeviceToHost, s));
+    PAES_CK(cudaMallocAsync(reinterpret_cast<void**>(&dd), b.total_bytes, s));
+    PAES_CK(cudaMemcpyAsync(dd, host, b.image_bytes, cudaMemcpyHostToDevice, s));
+    PAES_CK(cudaEventRecord(t_stage.ev, s));
+    PAES_CK(launch_batch(b.dec, batch_args(b, d_in, d_out, dd), d.sm_count, s));
+    if (b.check) {
+      auto* st = reinterpret_cast<std::uint32_t*>(host + b.status_off);
+      PAES_CK(cudaMemcpyAsync(st, dd + b.status_off, 4ull * n, cudaMemcpyDeviceToHost, s));
       PAES_CK(cudaFreeAsync(dd, s));
       PAES_CK(cudaStreamSynchronize(s));
-      bool bad = false;
-      for (uint32_t i = 0; i < n; ++i) {
-        const bool ok = st[i] != 0xffffffffu;
-        bad |= !ok;
-        if (out_lens) out_lens[i] = ok ? lens[i] - st[i] : UINT64_MAX;
-      }
-      if (bad) throw PaddingError("unpad: invalid pad bytes in one or more messages");
+      finish_lengths(b, st, out_lens);
     } else {
       PAES_CK(cudaFreeAsync(dd, s));
-      if (out_lens)
-        for (uint32_t i = 0; i < n; ++i) out_lens[i] = static_cast<uint64_t>(msgs[i].nblocks) * 16;
+      finish_lengths(b, nullptr, out_lens);
     }
     return PAES_OK;
   });
+}
+
+int paes_cuda_batch_plan_create(int dir, const uint64_t* in_off, const uint64_t* out_off, const uint64_t* lens,
+                                const uint8_t* rks, uint32_t n, int pad, int device_id, paes_batch_plan** plan) {
+  return guarded([&] {
+    if (!plan) throw std::invalid_argument("null plan pointer");
+    *plan = nullptr;
+    auto p = std::make_unique<paes_batch_plan>();
+    p->img = plan_batch(dir, in_off, out_off, lens, rks, n, pad);
+    p->device = device_id;
+    device(device_id);
+    DeviceGuard dg(device_id);
+    if (n) {
+      std::vector<std::uint8_t> host(p->img.image_bytes);
+      write_batch_image(p->img, in_off, out_off, rks, host.data());
+      PAES_CK(cudaMalloc(reinterpret_cast<void**>(&p->dd), p->img.total_bytes));
+      PAES_CK(cudaMemcpy(p->dd, host.data(), host.size(), cudaMemcpyHostToDevice));
+      if (p->img.check) PAES_CK(cudaMallocHost(reinterpret_cast<void**>(&p->h_status), 4ull * n));
+    }
+    *plan = p.release();
+    return PAES_OK;
+  });
+}
+
+int paes_cuda_batch_plan_run(paes_batch_plan* plan, const void* d_in, void* d_out, uint64_t* out_lens, void* stream) {
+  return guarded([&] {
+    if (!plan) throw std::invalid_argument("null plan");
+    const BatchImage& b = plan->img;
+    if (b.n == 0) return PAES_OK;
+    if (!d_in || !d_out) throw std::invalid_argument("null device buffer");
+    DevCtx& d = device(plan->device);
+    DeviceGuard dg(plan->device);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    PAES_CK(launch_batch(b.dec, batch_args(b, d_in, d_out, plan->dd), d.sm_count, s));
+    if (b.check) {
+      PAES_CK(cudaMemcpyAsync(plan->h_status, plan->dd + b.status_off, 4ull * b.n, cudaMemcpyDeviceToHost, s));
+      PAES_CK(cudaStreamSynchronize(s));
+      finish_lengths(b, plan->h_status, out_lens);
+    } else {
+      finish_lengths(b, nullptr, out_lens);
+    }
+    return PAES_OK;
+  });
+}
+
+void paes_cuda_batch_plan_destroy(paes_batch_plan* plan) {
+  if (!plan) return;
+  if (plan->dd) {
+    int prev = -1;
+    cudaGetDevice(&prev);
+    cudaSetDevice(plan->device);
+    cudaFree(plan->dd);
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+  if (plan->h_status) cudaFreeHost(plan->h_status);
+  delete plan;
 }
 
 int paes_cuda_sweep(uint64_t seed, uint64_t size, uint8_t* out) {
@@ -677,8 +833,8 @@ std::uint64_t file_shard(DevCtx& d, const Range& r, int in_fd, int out_fd, std::
                          const std::string& in_path, const std::string& out_path) {
   DeviceGuard g(d.id);
   ensure_pipeline(d, true);
-  const std::uint64_t C = d.chunk;
   const int S = static_cast<int>(d.st.size());
+  const std::uint64_t C = piece_size(r.in_len, d.chunk, S);
   const std::uint64_t npieces = std::max<std::uint64_t>(1, (r.in_len + C - 1) / C);
   std::vector<std::int64_t> pend_off(S, -1);
   std::vector<std::uint64_t> pend_len(S, 0);

@@ -273,14 +273,57 @@ def chunk_device(direction: int, d_in: int, nbytes: int, is_final: bool, rk: byt
     return olen.value
 
 
+def _u64_array(xs):
+    import numpy as np
+
+    a = np.ascontiguousarray(np.asarray(xs, dtype=np.uint64))
+    return a, a.ctypes.data_as(C.POINTER(C.c_uint64))
+
+
 def ecb_batch(direction: int, d_in: int, d_out: int, in_off, out_off, lens, rks: bytes, pad: bool, device: int = 0,
               stream: int = 0):
+    """One fused launch over n messages with per-message keys (config 5)."""
+    import numpy as np
+
     n = len(lens)
-    A = C.c_uint64 * max(n, 1)
-    olens = A()
-    _raise(N.load().paes_cuda_ecb_batch(direction, d_in, d_out, A(*in_off), A(*out_off), A(*lens), rks, n,
-                                        int(bool(pad)), olens, device, stream or None))
-    return list(olens[:n])
+    keep = [_u64_array(in_off), _u64_array(out_off), _u64_array(lens)]
+    olens = np.zeros(max(n, 1), dtype=np.uint64)
+    _raise(N.load().paes_cuda_ecb_batch(direction, d_in, d_out, keep[0][1], keep[1][1], keep[2][1], rks, n,
+                                        int(bool(pad)), olens.ctypes.data_as(C.POINTER(C.c_uint64)), device,
+                                        stream or None))
+    return olens[:n].tolist()
+
+
+class BatchPlan:
+    """Prepared batch (paes_cuda_batch_plan_*): descriptors and key words live
+    on the device; run() is a single launch."""
+
+    def __init__(self, direction: int, in_off, out_off, lens, rks: bytes, pad: bool, device: int = 0):
+        import numpy as np
+
+        self.n = len(lens)
+        self._olens = np.zeros(max(self.n, 1), dtype=np.uint64)
+        h = C.c_void_p()
+        a, b, c = _u64_array(in_off), _u64_array(out_off), _u64_array(lens)
+        _raise(N.load().paes_cuda_batch_plan_create(direction, a[1], b[1], c[1], rks, self.n, int(bool(pad)), device,
+                                                    C.byref(h)))
+        self._h = h
+
+    def run(self, d_in: int, d_out: int, stream: int = 0):
+        _raise(N.load().paes_cuda_batch_plan_run(self._h, d_in, d_out,
+                                                 self._olens.ctypes.data_as(C.POINTER(C.c_uint64)), stream or None))
+        return self._olens[: self.n].tolist()
+
+    def close(self):
+        if getattr(self, "_h", None) is not None and self._h.value:
+            N.load().paes_cuda_batch_plan_destroy(self._h)
+        self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 def sweep(seed: int, size: int) -> bytes:

@@ -390,3 +390,48 @@ def test_config5_batch_4096_messages(paes, gpu, digests):
     bad[176 * 7 + 160] ^= 0xFF
     with pytest.raises(paes.PaddingError):
         paes.ecb_batch(1, dst.data_ptr(), back.data_ptr(), out_off, in_off, [L + 16 for L in lens], bytes(bad), True)
+
+
+def test_batch_plan_small_ragged(paes, gpu, orc):
+    """Prepared-plan batch == per-message reference transforms, ragged lengths,
+    messages shorter than a warp tile, decrypt with trailer checks."""
+    torch = _torch()
+    rnd = random.Random(55)
+    n = 300
+    lens = [rnd.choice([0, 1, 15, 16, 17, 100, 511, 512, 1000, 4096, 7777, 70000]) for _ in range(n)]
+    in_off, out_off, oi, oo = [], [], 0, 0
+    for L in lens:
+        in_off.append(oi)
+        out_off.append(oo)
+        oi += (L + 15) // 16 * 16 + 16
+        oo += (L // 16 + 1) * 16
+    keys = [os.urandom(16) for _ in range(n)]
+    rks = b"".join(paes.round_keys(k) for k in keys)
+    msgs = [os.urandom(L) for L in lens]
+    host = bytearray(oi)
+    for i, m in enumerate(msgs):
+        host[in_off[i]:in_off[i] + len(m)] = m
+    src = torch.frombuffer(host, dtype=torch.uint8).cuda()
+    dst = torch.zeros(oo + 16, dtype=torch.uint8, device="cuda")
+    plan = paes.BatchPlan(0, in_off, out_off, lens, rks, True)
+    olens = plan.run(src.data_ptr(), dst.data_ptr())
+    torch.cuda.synchronize()
+    out = dst.cpu().numpy().tobytes()
+    for i in range(n):
+        want = orc.encrypt_chunk(msgs[i], True, keys[i])
+        assert olens[i] == len(want)
+        assert out[out_off[i]:out_off[i] + len(want)] == want, i
+    # one-shot API gives the same bytes
+    dst2 = torch.zeros_like(dst)
+    assert paes.ecb_batch(0, src.data_ptr(), dst2.data_ptr(), in_off, out_off, lens, rks, True) == olens
+    assert paes.count_mismatch_device(dst.data_ptr(), dst2.data_ptr(), oo) == 0
+    # decrypt back with trailer checks
+    back = torch.zeros(oo + 16, dtype=torch.uint8, device="cuda")
+    dplan = paes.BatchPlan(1, out_off, out_off, olens, rks, True)
+    plens = dplan.run(dst.data_ptr(), back.data_ptr())
+    assert plens == lens
+    bb = back.cpu().numpy().tobytes()
+    for i in range(n):
+        assert bb[out_off[i]:out_off[i] + lens[i]] == msgs[i]
+    plan.close()
+    dplan.close()
