@@ -238,7 +238,7 @@ def run_reference(args, dist: Dist):
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(1e3 * total / args.steps, 3), "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "u8", "data": "synthetic (counter stream, seed 3)",
-        "config": workload_config(args),
+        "config": workload_config(args, "reference"),
         "cpu_baseline": {"value": round(value, 4), "unit": "GB/s", "cores": workers, "physical_cores": phys,
                          "kind": "reference", "sample": sample,
                          "step_seconds": [round(x, 4) for x in times]},
@@ -262,11 +262,15 @@ def cpu_baseline(args):
             "seconds": [round(x, 4) for x in samples]}
 
 
-def workload_config(args):
-    return {"workload": f"config4: {args.total_bytes} B counter-stream (seed {args.seed}) AES-128 encrypt, "
-                        f"PKCS#7 always-pad, plan_chunks block-range shards",
-            "total_bytes": args.total_bytes, "parallelism": f"dp{args.gpus} (contiguous block ranges, no collective)",
-            "l2": "inputs >> L2 (126 MB); no flush needed", "step": "one kernel launch over the rank's shard"}
+def workload_config(args, impl: str = "b200"):
+    cfg = {"workload": f"config4: {args.total_bytes} B counter-stream (seed {args.seed}) AES-128 encrypt, "
+                       f"PKCS#7 always-pad, plan_chunks block-range shards",
+           "total_bytes": args.total_bytes, "parallelism": f"dp{args.gpus} (contiguous block ranges, no collective)"}
+    if impl == "b200":
+        cfg.update(l2="inputs >> L2 (126 MB); no flush needed", step="one kernel launch over the rank's shard")
+    else:
+        cfg.update(step="one reference pthreads pass (plan_chunks over all host threads) over a bounded sample")
+    return cfg
 
 
 # --------------------------------------------------------------------- B200 arm

@@ -9,6 +9,7 @@
 // IoError -> PAES_EIO, WorkerError -> PAES_EWORKER, CUDA -> PAES_ECUDA.
 #include <cuda_runtime.h>
 #include <fcntl.h>
+#include <sys/mman.h>
 #include <sys/stat.h>
 #include <unistd.h>
 
@@ -806,6 +807,14 @@ struct IoFail {
   std::string msg;
 };
 
+struct Map {
+  std::uint8_t* p = nullptr;
+  std::uint64_t n = 0;
+  ~Map() {
+    if (p) ::munmap(p, n);
+  }
+};
+
 void pread_all(int fd, std::uint8_t* p, std::uint64_t n, std::uint64_t off, const std::string& path) {
   std::uint64_t got = 0;
   while (got < n) {
@@ -826,11 +835,50 @@ void pwrite_all(int fd, const std::uint8_t* p, std::uint64_t n, std::uint64_t of
   }
 }
 
+// Split one pread/pwrite of a pinned slot across several host threads: a
+// single thread copying from/to the page cache runs at a few GB/s, far below
+// the PCIe rate the slot is DMA'd at.  Threads per shard = host threads /
+// shards, at most 8.
+unsigned g_io_threads_per_shard = 0;  // 0 = auto
+
+template <class F>
+void par_io(std::uint64_t n, unsigned threads, F&& f) {
+  constexpr std::uint64_t kGrain = 4ull << 20;
+  const std::uint64_t parts = std::min<std::uint64_t>(threads, (n + kGrain - 1) / kGrain);
+  if (parts <= 1) {
+    f(0, n);
+    return;
+  }
+  const std::uint64_t step = ((n / parts) + 4095) & ~std::uint64_t(4095);
+  std::vector<std::thread> pool;
+  std::vector<std::string> errs(parts);
+  for (std::uint64_t i = 1; i < parts; ++i) {
+    const std::uint64_t b = std::min(n, i * step), e = std::min(n, (i + 1) * step);
+    if (b >= e) break;
+    pool.emplace_back([&, i, b, e] {
+      try {
+        f(b, e - b);
+      } catch (const IoFail& x) {
+        errs[i] = x.msg;
+      }
+    });
+  }
+  try {
+    f(0, std::min(n, step));
+  } catch (const IoFail& x) {
+    errs[0] = x.msg;
+  }
+  for (auto& t : pool) t.join();
+  for (const auto& e : errs)
+    if (!e.empty()) throw IoFail{e};
+}
+
 // One GPU's shard of a file job: pread into pinned slots, H2D, kernel, D2H
 // back into the same slot, pwrite -- all slots in flight at once.  Returns
 // the output bytes written (decrypt final: unpadded).
-std::uint64_t file_shard(DevCtx& d, const Range& r, int in_fd, int out_fd, std::uint64_t off, const KeyWords& kw,
-                         const std::string& in_path, const std::string& out_path) {
+std::uint64_t file_shard(DevCtx& d, const Range& r, int in_fd, int out_fd, std::uint8_t* out_map, std::uint64_t off,
+                         const KeyWords& kw, const std::string& in_path, const std::string& out_path,
+                         unsigned io_threads) {
   DeviceGuard g(d.id);
   ensure_pipeline(d, true);
   const int S = static_cast<int>(d.st.size());
@@ -841,7 +889,13 @@ std::uint64_t file_shard(DevCtx& d, const Range& r, int in_fd, int out_fd, std::
   auto drain = [&](int s) {
     if (pend_off[s] < 0) return;
     PAES_CK(cudaEventSynchronize(d.ev[s]));
-    pwrite_all(out_fd, d.hbuf[s], pend_len[s], static_cast<std::uint64_t>(pend_off[s]), out_path);
+    const std::uint64_t base = static_cast<std::uint64_t>(pend_off[s]);
+    std::uint8_t* slot = d.hbuf[s];
+    if (out_map)  // page faults of a shared mapping proceed in parallel; pwrite serialises on the inode
+      par_io(pend_len[s], io_threads, [&](std::uint64_t o, std::uint64_t n) { std::memcpy(out_map + base + o, slot + o, n); });
+    else
+      par_io(pend_len[s], io_threads,
+             [&](std::uint64_t o, std::uint64_t n) { pwrite_all(out_fd, slot + o, n, base + o, out_path); });
     pend_off[s] = -1;
   };
   std::uint64_t out_total = 0;
@@ -851,7 +905,9 @@ std::uint64_t file_shard(DevCtx& d, const Range& r, int in_fd, int out_fd, std::
     const std::uint64_t poff = k * C;
     const std::uint64_t len = std::min<std::uint64_t>(C, r.in_len - poff);
     const bool last = k + 1 == npieces;
-    if (len) pread_all(in_fd, d.hbuf[s], len, off + poff, in_path);
+    std::uint8_t* slot = d.hbuf[s];
+    par_io(len, io_threads,
+           [&](std::uint64_t o, std::uint64_t n) { pread_all(in_fd, slot + o, n, off + poff + o, in_path); });
     EcbArgs a = make_args(r, d.dbuf[s], d.dbuf[s], len, last, kw, d.d_status);
     if (len) PAES_CK(cudaMemcpyAsync(d.dbuf[s], d.hbuf[s], len, cudaMemcpyHostToDevice, d.st[s]));
     if (a.check_pad) PAES_CK(cudaMemsetAsync(d.d_status, 0xff, 4, d.st[s]));
@@ -898,8 +954,19 @@ extern "C" int paes_cuda_run_job(const char* input_path, const char* output_path
     const KeyWords kw = dec ? dec_key_words(rk) : enc_key_words(rk);
     tmp = out_path + ".part." + std::to_string(::getpid());
     Fd out;
-    out.fd = ::open(tmp.c_str(), O_WRONLY | O_CREAT | O_TRUNC, 0644);
+    out.fd = ::open(tmp.c_str(), O_RDWR | O_CREAT | O_TRUNC, 0644);
     if (out.fd < 0) return fail(PAES_EIO, "cannot open output: " + tmp);
+    // Output through a shared mapping sized to the worst case (trimmed after
+    // a decrypt's unpad); plain pwrite if the file system refuses mmap.
+    const std::uint64_t cap = dec ? len : (len / 16 + 1) * 16;
+    Map map;
+    if (cap && ::ftruncate(out.fd, static_cast<off_t>(cap)) == 0) {
+      void* p = ::mmap(nullptr, cap, PROT_READ | PROT_WRITE, MAP_SHARED, out.fd, 0);
+      if (p != MAP_FAILED) {
+        map.p = static_cast<std::uint8_t*>(p);
+        map.n = cap;
+      }
+    }
     std::vector<std::uint64_t> produced(plan.size(), 0);
     std::vector<std::string> failures(plan.size());
     auto work = [&](std::size_t i) {
@@ -912,7 +979,11 @@ extern "C" int paes_cuda_run_job(const char* input_path, const char* output_path
       try {
         DevCtx& d = device(devs[i]);
         std::lock_guard<std::mutex> lk(d.mu);
-        produced[i] = file_shard(d, r, in.fd, out.fd, c.offset, kw, in_path, tmp);
+        const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+        const unsigned io = g_io_threads_per_shard
+                                ? g_io_threads_per_shard
+                                : std::clamp<unsigned>(hw / static_cast<unsigned>(plan.size()), 1u, 8u);
+        produced[i] = file_shard(d, r, in.fd, out.fd, map.p, c.offset, kw, in_path, tmp, io);
       } catch (const CudaFail& e) {
         failures[i] = e.msg;
       } catch (const IoFail& e) {

@@ -435,3 +435,36 @@ def test_batch_plan_small_ragged(paes, gpu, orc):
         assert bb[out_off[i]:out_off[i] + lens[i]] == msgs[i]
     plan.close()
     dplan.close()
+
+
+def test_multi_shard_paths_on_one_device(paes, gpu, orc, tmp_path):
+    """The multi-GPU sharder (plan_chunks over the device list, one host thread
+    per shard, WorkerError aggregation) exercised with device 0 listed three
+    times: same code path as 3 GPUs, shards serialise on the device lock."""
+    paes.set_devices([0, 0, 0])
+    try:
+        key = os.urandom(16)
+        for n in [0, 15, 16, 47, 48, 49, 1000, 100_003, 3 * 4096 + 5]:
+            data = os.urandom(n)
+            ct = paes.encrypt_chunk(data, True, key, ngpus=3)
+            assert ct == orc.encrypt_chunk(data, True, key), n
+            assert paes.decrypt_chunk(ct, True, key, ngpus=3) == data
+            if n % 16 == 0:
+                assert paes.encrypt_ecb(data, key, ngpus=3) == orc.ecb(0, data, key)
+        # wrong key on a sharded buffer decrypt -> PaddingError (decrypt_chunk semantics)
+        ct = paes.encrypt_bytes(os.urandom(5000), key)
+        with pytest.raises(paes.PaddingError):
+            paes.decrypt_chunk(ct, True, bytes([key[0] ^ 1]) + key[1:], ngpus=3)
+        # files: 3 shards, wrong key names the final chunk (exec.cpp:177-184)
+        data = os.urandom(200_001)
+        (tmp_path / "p").write_bytes(data)
+        o = paes.encrypt_file(str(tmp_path / "p"), str(tmp_path / "c"), key, workers=3)
+        assert o["bytes_out"] == (len(data) // 16 + 1) * 16
+        assert (tmp_path / "c").read_bytes() == orc.encrypt_chunk(data, True, key)
+        paes.decrypt_file(str(tmp_path / "c"), str(tmp_path / "d"), key, workers=3)
+        assert (tmp_path / "d").read_bytes() == data
+        with pytest.raises(paes.WorkerError, match="chunk 2"):
+            paes.decrypt_file(str(tmp_path / "c"), str(tmp_path / "bad"), bytes([key[0] ^ 1]) + key[1:], workers=3)
+        assert not (tmp_path / "bad").exists()
+    finally:
+        paes.set_devices([])
