@@ -139,6 +139,15 @@ int paes_cuda_ecb_batch(int dir, const void* d_in, void* d_out, const uint64_t* 
  * exec.cpp:148, 368); each run is then one launch over any buffers with that
  * layout.  Same semantics as paes_cuda_ecb_batch.  A plan may be run from one
  * thread at a time. */
+/* Host-pointer batch (config 5 end to end): message i = h_in[in_off[i] ..
+ * +lens[i]) -> h_out[out_off[i] ..], same rules as paes_cuda_ecb_batch.
+ * Consecutive messages are grouped into ~staging-chunk-sized groups; each
+ * group is one H2D of its input span, one fused launch, one D2H, with the
+ * groups pipelined over the device's stream ring.  Synchronous. */
+int paes_cuda_batch_host(int dir, const uint8_t* h_in, uint8_t* h_out, const uint64_t* in_off, const uint64_t* out_off,
+                         const uint64_t* lens, const uint8_t* rks, uint32_t n, int pad, uint64_t* out_lens,
+                         int device);
+
 typedef struct paes_batch_plan paes_batch_plan;
 int paes_cuda_batch_plan_create(int dir, const uint64_t* in_off, const uint64_t* out_off, const uint64_t* lens,
                                 const uint8_t* rks, uint32_t n, int pad, int device, paes_batch_plan** plan);

@@ -490,7 +490,7 @@ struct BatchImage {
   bool dec = false, check = false;
   std::uint32_t n = 0;
   unsigned long long total_tiles = 0;  // warp tiles (each message owns whole tiles)
-  std::size_t msg_bytes = 0, image_bytes = 0, status_off = 0, total_bytes = 0;
+  std::size_t msg_bytes = 0, keys_off = 0, image_bytes = 0, status_off = 0, total_bytes = 0;
   std::vector<std::uint64_t> lens;
   std::vector<std::uint32_t> nblocks;
 };
@@ -504,7 +504,8 @@ BatchImage plan_batch(int dir, const uint64_t* in_off, const uint64_t* out_off, 
   b.check = b.dec && pad;
   b.n = n;
   b.msg_bytes = sizeof(BatchMsg) * n;
-  b.image_bytes = b.msg_bytes + sizeof(KeyWords) * n;
+  b.keys_off = (b.msg_bytes + 255) & ~std::size_t(255);  // 16-byte key loads need alignment
+  b.image_bytes = b.keys_off + sizeof(KeyWords) * n;
   b.status_off = (b.image_bytes + 255) & ~std::size_t(255);
   b.total_bytes = b.status_off + (b.check ? 4ull * n : 0);
   b.lens.assign(lens, lens + n);
@@ -524,7 +525,7 @@ BatchImage plan_batch(int dir, const uint64_t* in_off, const uint64_t* out_off, 
 void write_batch_image(const BatchImage& b, const uint64_t* in_off, const uint64_t* out_off, const uint8_t* rks,
                        std::uint8_t* dst) {
   auto* msgs = reinterpret_cast<BatchMsg*>(dst);
-  auto* keys = reinterpret_cast<KeyWords*>(dst + b.msg_bytes);
+  auto* keys = reinterpret_cast<KeyWords*>(dst + b.keys_off);
   unsigned long long tile = 0;
   for (uint32_t i = 0; i < b.n; ++i) {
     BatchMsg m{};
@@ -545,7 +546,7 @@ BatchArgs batch_args(const BatchImage& b, const void* d_in, void* d_out, std::ui
   a.in = static_cast<const std::uint8_t*>(d_in);
   a.out = static_cast<std::uint8_t*>(d_out);
   a.msgs = reinterpret_cast<const BatchMsg*>(dd);
-  a.keys = reinterpret_cast<const std::uint32_t*>(dd + b.msg_bytes);
+  a.keys = reinterpret_cast<const std::uint32_t*>(dd + b.keys_off);
   a.status = b.check ? reinterpret_cast<std::uint32_t*>(dd + b.status_off) : nullptr;
   a.total_tiles = b.total_tiles;
   a.nmsg = b.n;
@@ -696,6 +697,104 @@ void paes_cuda_batch_plan_destroy(paes_batch_plan* plan) {
   }
   if (plan->h_status) cudaFreeHost(plan->h_status);
   delete plan;
+}
+
+// Host-pointer batch: consecutive messages are grouped into ~chunk-sized
+// groups; per group one H2D of its input span, one batch launch over
+// group-relative descriptors, one D2H of its output span, the groups
+// round-robin over the device's stream ring so copies overlap compute.
+int paes_cuda_batch_host(int dir, const uint8_t* h_in, uint8_t* h_out, const uint64_t* in_off, const uint64_t* out_off,
+                         const uint64_t* lens, const uint8_t* rks, uint32_t n, int pad, uint64_t* out_lens,
+                         int device_id) {
+  return guarded([&] {
+    const BatchImage all = plan_batch(dir, in_off, out_off, lens, rks, n, pad);
+    if (n == 0) return PAES_OK;
+    if (!h_in || !h_out) throw std::invalid_argument("null host buffer");
+    DevCtx& d = device(device_id);
+    DeviceGuard dg(device_id);
+    std::lock_guard<std::mutex> lk(d.mu);
+    ensure_pipeline(d, false);
+    const std::uint64_t C = d.chunk;
+    const int S = static_cast<int>(d.st.size());
+    // groups of consecutive messages whose input and output spans stay <= C
+    struct Group {
+      std::uint32_t first, count;
+      std::uint64_t in_lo, in_hi, out_lo, out_hi;
+    };
+    std::vector<Group> groups;
+    for (std::uint32_t i = 0; i < n; ++i) {
+      const std::uint64_t ilo = in_off[i], ihi = in_off[i] + lens[i];
+      const std::uint64_t olo = out_off[i], ohi = out_off[i] + 16ull * all.nblocks[i];
+      if (!groups.empty()) {
+        Group& g = groups.back();
+        const std::uint64_t nil = std::min(g.in_lo, ilo), nih = std::max(g.in_hi, ihi);
+        const std::uint64_t nol = std::min(g.out_lo, olo), noh = std::max(g.out_hi, ohi);
+        if (nih - nil <= C && noh - nol <= C) {
+          g.count += 1;
+          g.in_lo = nil, g.in_hi = nih, g.out_lo = nol, g.out_hi = noh;
+          continue;
+        }
+      }
+      groups.push_back({i, 1, ilo, ihi, olo, ohi});
+    }
+    // one pinned image for every group's descriptors (+ status words)
+    std::vector<std::size_t> img_off(groups.size());
+    std::vector<BatchImage> imgs;
+    imgs.reserve(groups.size());
+    std::size_t total = 0;
+    std::vector<std::uint64_t> rin(n), rout(n);
+    for (std::size_t k = 0; k < groups.size(); ++k) {
+      const Group& g = groups[k];
+      for (std::uint32_t i = g.first; i < g.first + g.count; ++i) {
+        rin[i] = in_off[i] - g.in_lo;
+        rout[i] = out_off[i] - g.out_lo;
+      }
+      imgs.push_back(plan_batch(dir, rin.data() + g.first, rout.data() + g.first, lens + g.first,
+                                rks + 176ull * g.first, g.count, pad));
+      img_off[k] = total;
+      total += (imgs.back().total_bytes + 255) & ~std::size_t(255);
+    }
+    std::uint8_t* host = staging(total, device_id);
+    for (std::size_t k = 0; k < groups.size(); ++k) {
+      const Group& g = groups[k];
+      write_batch_image(imgs[k], rin.data() + g.first, rout.data() + g.first, rks + 176ull * g.first,
+                        host + img_off[k]);
+    }
+    for (std::size_t k = 0; k < groups.size(); ++k) {
+      const Group& g = groups[k];
+      const BatchImage& b = imgs[k];
+      cudaStream_t s = d.st[k % S];
+      std::uint8_t *din = nullptr, *dout = nullptr, *dd = nullptr;
+      PAES_CK(cudaMallocAsync(reinterpret_cast<void**>(&din), std::max<std::uint64_t>(16, g.in_hi - g.in_lo), s));
+      PAES_CK(cudaMallocAsync(reinterpret_cast<void**>(&dout), std::max<std::uint64_t>(16, g.out_hi - g.out_lo), s));
+      PAES_CK(cudaMallocAsync(reinterpret_cast<void**>(&dd), b.total_bytes, s));
+      if (g.in_hi > g.in_lo)
+        PAES_CK(cudaMemcpyAsync(din, h_in + g.in_lo, g.in_hi - g.in_lo, cudaMemcpyHostToDevice, s));
+      PAES_CK(cudaMemcpyAsync(dd, host + img_off[k], b.image_bytes, cudaMemcpyHostToDevice, s));
+      PAES_CK(launch_batch(b.dec, batch_args(b, din, dout, dd), d.sm_count, s));
+      PAES_CK(cudaMemcpyAsync(h_out + g.out_lo, dout, g.out_hi - g.out_lo, cudaMemcpyDeviceToHost, s));
+      if (b.check)
+        PAES_CK(cudaMemcpyAsync(host + img_off[k] + b.status_off, dd + b.status_off, 4ull * b.n,
+                                cudaMemcpyDeviceToHost, s));
+      PAES_CK(cudaFreeAsync(din, s));
+      PAES_CK(cudaFreeAsync(dout, s));
+      PAES_CK(cudaFreeAsync(dd, s));
+    }
+    for (auto s : d.st) PAES_CK(cudaStreamSynchronize(s));
+    PAES_CK(cudaEventRecord(t_stage.ev, d.st[0]));
+    bool bad = false;
+    for (std::size_t k = 0; k < groups.size(); ++k) {
+      const BatchImage& b = imgs[k];
+      try {
+        finish_lengths(b, b.check ? reinterpret_cast<const std::uint32_t*>(host + img_off[k] + b.status_off) : nullptr,
+                       out_lens ? out_lens + groups[k].first : nullptr);
+      } catch (const PaddingError&) {
+        bad = true;
+      }
+    }
+    if (bad) throw PaddingError("unpad: invalid pad bytes in one or more messages");
+    return PAES_OK;
+  });
 }
 
 int paes_cuda_sweep(uint64_t seed, uint64_t size, uint8_t* out) {

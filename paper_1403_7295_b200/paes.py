@@ -294,6 +294,20 @@ def ecb_batch(direction: int, d_in: int, d_out: int, in_off, out_off, lens, rks:
     return olens[:n].tolist()
 
 
+def ecb_batch_host(direction: int, h_in: int, h_out: int, in_off, out_off, lens, rks: bytes, pad: bool,
+                   device: int = 0):
+    """Host-pointer batch (paes_cuda_batch_host): grouped, pipelined H2D /
+    fused launch / D2H.  h_in / h_out are host addresses (pinned for speed)."""
+    import numpy as np
+
+    n = len(lens)
+    keep = [_u64_array(in_off), _u64_array(out_off), _u64_array(lens)]
+    olens = np.zeros(max(n, 1), dtype=np.uint64)
+    _raise(N.load().paes_cuda_batch_host(direction, h_in, h_out, keep[0][1], keep[1][1], keep[2][1], rks, n,
+                                         int(bool(pad)), olens.ctypes.data_as(C.POINTER(C.c_uint64)), device))
+    return olens[:n].tolist()
+
+
 class BatchPlan:
     """Prepared batch (paes_cuda_batch_plan_*): descriptors and key words live
     on the device; run() is a single launch."""
