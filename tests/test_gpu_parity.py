@@ -500,3 +500,46 @@ def test_batch_host_pipeline(paes, gpu, orc):
             assert back[out_off[i]:out_off[i] + lens[i]].tobytes() == hin[in_off[i]:in_off[i] + lens[i]].tobytes()
     finally:
         paes.set_pipeline(64 * MiB, 3)
+
+
+def test_no_writes_outside_outputs(paes, gpu, orc):
+    """Guard bands (compute-sanitizer is unavailable on this pool): every
+    output region is surrounded by 4 KiB of canary bytes that must survive
+    the single-key, unaligned, in-place and batch kernels."""
+    torch = _torch()
+    G = 4096
+    key = os.urandom(16)
+    rk = paes.round_keys(key)
+    for n in [0, 1, 15, 16, 17, 1023, 1024, 1025, 65536 + 3, 1 << 20]:
+        data = os.urandom(n)
+        for direction in (0, 1):
+            inp = data if direction == 0 else orc.encrypt_chunk(data, True, key)
+            m = len(inp) if direction == 1 else (n // 16 + 1) * 16
+            for off in (0, 3):
+                src = dev_from_bytes(inp, offset=off)
+                buf = torch.full((G + off + m + G,), 0xA5, dtype=torch.uint8, device="cuda")
+                got = paes.chunk_device(direction, src.data_ptr() + off, len(inp), True, rk, buf.data_ptr() + G + off)
+                torch.cuda.synchronize()
+                host = buf.cpu().numpy()
+                assert (host[:G + off] == 0xA5).all(), (n, direction, off, "underrun")
+                assert (host[G + off + m:] == 0xA5).all(), (n, direction, off, "overrun")
+                assert got == (m if direction == 0 else n)
+    # batch: canaries between messages
+    lens = [0, 5, 16, 100, 4096, 12345]
+    keys = [os.urandom(16) for _ in lens]
+    rks = b"".join(paes.round_keys(k) for k in keys)
+    in_off, out_off, oi, oo = [], [], 0, G
+    for L in lens:
+        in_off.append(oi)
+        oi += (L + 15) // 16 * 16 + 16
+        out_off.append(oo)
+        oo += (L // 16 + 1) * 16 + G
+    src = torch.frombuffer(bytearray(os.urandom(oi)), dtype=torch.uint8).cuda()
+    dst = torch.full((oo,), 0xA5, dtype=torch.uint8, device="cuda")
+    olens = paes.ecb_batch(0, src.data_ptr(), dst.data_ptr(), in_off, out_off, lens, rks, True)
+    torch.cuda.synchronize()
+    host = dst.cpu().numpy()
+    mask = np.ones(oo, dtype=bool)
+    for o, L in zip(out_off, olens):
+        mask[o:o + L] = False
+    assert (host[mask] == 0xA5).all()
