@@ -21,3 +21,10 @@ cudaError_t launch_mismatch(const void* a, const void* b, unsigned long long nbl
 unsigned long long launch_count();
 
 }  // namespace paes_b200
+
+namespace paes_b200 {
+// Experimental bitsliced encrypt (aes_bitsliced.cu): the LOP3 alternative of
+// the north_star A/B.  Whole 1024-block tiles only.
+cudaError_t launch_ecb_bitsliced_experiment(const std::uint8_t* in, std::uint8_t* out, unsigned long long nblocks,
+                                            const KeyWords& kw, int sm_count, cudaStream_t stream);
+}  // namespace paes_b200

@@ -1161,3 +1161,17 @@ extern "C" int paes_cuda_run_job(const char* input_path, const char* output_path
   if (rc != PAES_OK && !tmp.empty()) ::unlink(tmp.c_str());  // no partial output (exec.cpp:86-91)
   return rc;
 }
+
+// Experimental, not in include/paes_cuda.h: the bitsliced (LOP3) encrypt
+// kernel for the T-table vs bitsliced A/B (scripts/bitsliced_ab.py).
+extern "C" int paes_cuda_experimental_bitsliced_ecb(const void* d_in, void* d_out, uint64_t len, const uint8_t rk[176],
+                                                    int device_id, void* stream) {
+  return guarded([&] {
+    if (len % (16 * 1024)) throw std::invalid_argument("length must be a multiple of 16 KiB");
+    DevCtx& d = device(device_id);
+    DeviceGuard g(device_id);
+    PAES_CK(launch_ecb_bitsliced_experiment(static_cast<const std::uint8_t*>(d_in), static_cast<std::uint8_t*>(d_out),
+                                            len / 16, enc_key_words(rk), d.sm_count, static_cast<cudaStream_t>(stream)));
+    return PAES_OK;
+  });
+}
