@@ -279,7 +279,7 @@ def run_b200(args, dist: Dist):
 
     from paper_1403_7295_b200 import paes
 
-    dev = dist.local
+    dev = 0 if os.environ.get("PAES_BENCH_SHARED_DEVICE") == "1" else dist.local
     torch.cuda.set_device(dev)
     paes.set_devices([dev])
     N = dist.world
@@ -449,7 +449,11 @@ def main():
     args = ap.parse_args()
     if args.warmup < 3 and os.environ.get("PAES_BENCH_ALLOW_SHORT") != "1":
         args.warmup = 3  # contract: >= 3 warm-up steps
-    dist = Dist(args.gpus)
+    # PAES_BENCH_SHARED_DEVICE=1: every rank on cuda:0 over gloo -- a plumbing
+    # smoke of the N>1 path on a one-GPU box (ranks never wait on each other's
+    # kernels; only CPU barriers and scalar reductions cross ranks).
+    shared = os.environ.get("PAES_BENCH_SHARED_DEVICE") == "1"
+    dist = Dist(args.gpus, backend="gloo" if shared else "nccl")
     try:
         if args.impl == "reference":
             res = run_reference(args, dist)
