@@ -289,7 +289,7 @@ def run_b200(args, dist: Dist):
     key = paes.sweep(args.seed, 16)
     rk = paes.round_keys(key)
     stream = torch.cuda.Stream(device=dev)
-    pt = torch.empty(max(n, 16), dtype=torch.uint8, device=dev)
+    pt = torch.empty(max(n, 16) + 16, dtype=torch.uint8, device=dev)  # + room for a decrypted pad block
     ct = torch.empty(max(out_n, 16) + 16, dtype=torch.uint8, device=dev)
     with torch.cuda.stream(stream):
         paes.counter_fill_device(args.seed, off, n - n % 8, pt.data_ptr(), dev, stream.cuda_stream)
@@ -371,6 +371,43 @@ def run_b200(args, dist: Dist):
         "frac_of_binding": round(pt_gbs / min(pipe_peak, hbm_pt_bound), 4),
     }
 
+    # decrypt direction on the ciphertext just produced (the inverse-round
+    # kernel; a final shard also runs the trailer check + its readback)
+    dec = None
+    if not args.no_decrypt and out_n:
+        # decrypt into the plaintext buffer (three 64 GiB buffers do not fit);
+        # the round trip is checked by the position-keyed checksum of pt
+        cs_pt = paes.checksum_device(pt.data_ptr(), n - n % 8, off // 8, dev, stream.cuda_stream)
+        back = pt
+
+        def dstep():
+            return paes.chunk_device(1, ct.data_ptr(), out_n, is_final, rk, back.data_ptr(), dev, stream.cuda_stream)
+
+        for _ in range(args.warmup):
+            dstep()
+        stream.synchronize()
+        devs_ = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+        dist.barrier()
+        torch.cuda.synchronize(dev)
+        d0, d1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        d0.record(stream)
+        for i in range(args.steps):
+            devs_[i][0].record(stream)
+            got = dstep()
+            devs_[i][1].record(stream)
+        d1.record(stream)
+        torch.cuda.synchronize(dev)
+        dist.barrier()
+        assert got == n, (got, n)
+        ok = paes.checksum_device(pt.data_ptr(), n - n % 8, off // 8, dev, stream.cuda_stream) == cs_pt
+        dmax = dist.reduce(float(d0.elapsed_time(d1)), "max")
+        dtot = dist.reduce(int(out_n), "sum")
+        dk = statistics.mean(a.elapsed_time(b) for a, b in devs_) / 1e3
+        dec = {"value": round(dtot * args.steps / (dmax / 1e3) / 1e9, 2), "unit": "GB/s",
+               "ms_per_step": round(dmax / args.steps, 4), "kernel": "ecb_kernel<dec> (Td tables + InvS, smem x32)",
+               "pipe_frac": round(out_n / dk / 1e9 / pipe_peak, 4),
+               "round_trip": "ok (plaintext checksum restored)" if ok else "MISMATCH"}
+
     # e2e through the public host-pointer API (pinned host memory)
     e2e = None
     if not args.no_e2e and n:
@@ -382,7 +419,7 @@ def run_b200(args, dist: Dist):
         "scaling": "strong", "vs_baseline": None, "published_reference_cpu_gbs": PUBLISHED_CPU_GBS,
         "dtype": "u8", "data": "synthetic (counter stream generated on device, seed 3; key = sweep(3,16))",
         "config": workload_config(args), "parity": parity, "roofline": roofline, "clocks": clocks,
-        "gpu_launches": launches, "e2e": e2e, "device": props.name,
+        "gpu_launches": launches, "e2e": e2e, "decrypt": dec, "device": props.name,
     }
     return result
 
@@ -445,6 +482,7 @@ def main():
     ap.add_argument("--seed", type=int, default=3)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-decrypt", action="store_true")
     ap.add_argument("--ref-step-s", type=float, default=3.0, help="seconds of CPU work per reference step")
     args = ap.parse_args()
     if args.warmup < 3 and os.environ.get("PAES_BENCH_ALLOW_SHORT") != "1":
