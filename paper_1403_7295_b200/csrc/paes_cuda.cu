@@ -1100,24 +1100,42 @@ std::uint64_t file_shard(DevCtx& d, const Range& r, int in_fd, int out_fd, std::
   const int S = static_cast<int>(d.st.size());
   const std::uint64_t C = piece_size(r.in_len, d.chunk, S);
   const std::uint64_t npieces = std::max<std::uint64_t>(1, (r.in_len + C - 1) / C);
-  std::vector<std::int64_t> pend_off(S, -1);
-  std::vector<std::uint64_t> pend_len(S, 0);
-  auto drain = [&](int s) {
-    if (pend_off[s] < 0) return;
-    PAES_CK(cudaEventSynchronize(d.ev[s]));
-    const std::uint64_t base = static_cast<std::uint64_t>(pend_off[s]);
-    std::uint8_t* slot = d.hbuf[s];
-    if (out_map)  // page faults of a shared mapping proceed in parallel; pwrite serialises on the inode
-      par_io(pend_len[s], io_threads, [&](std::uint64_t o, std::uint64_t n) { std::memcpy(out_map + base + o, slot + o, n); });
-    else
-      par_io(pend_len[s], io_threads,
-             [&](std::uint64_t o, std::uint64_t n) { pwrite_all(out_fd, slot + o, n, base + o, out_path); });
-    pend_off[s] = -1;
+  // Each slot's output is written back by its own writer thread (it waits on
+  // the slot's event, then copies into the output mapping), so writing piece
+  // k-1 overlaps reading piece k; a slot is refilled only after its writer
+  // has been joined.
+  std::vector<std::thread> writer(S);
+  std::vector<std::string> werr(S);
+  auto write_slot = [&](int s, std::uint64_t base, std::uint64_t len) {
+    try {
+      PAES_CK(cudaSetDevice(d.id));
+      PAES_CK(cudaEventSynchronize(d.ev[s]));
+      std::uint8_t* slot = d.hbuf[s];
+      if (out_map)  // page faults of a shared mapping proceed in parallel; pwrite serialises on the inode
+        par_io(len, io_threads, [&](std::uint64_t o, std::uint64_t n) { std::memcpy(out_map + base + o, slot + o, n); });
+      else
+        par_io(len, io_threads, [&](std::uint64_t o, std::uint64_t n) { pwrite_all(out_fd, slot + o, n, base + o, out_path); });
+    } catch (const IoFail& e) {
+      werr[s] = e.msg;
+    } catch (const CudaFail& e) {
+      werr[s] = e.msg;
+    }
   };
+  auto join_slot = [&](int s) {
+    if (writer[s].joinable()) writer[s].join();
+    if (!werr[s].empty()) throw IoFail{werr[s]};
+  };
+  struct JoinAll {  // never leave a writer running on an exception
+    std::vector<std::thread>& w;
+    ~JoinAll() {
+      for (auto& t : w)
+        if (t.joinable()) t.join();
+    }
+  } join_all{writer};
   std::uint64_t out_total = 0;
   for (std::uint64_t k = 0; k < npieces; ++k) {
     const int s = static_cast<int>(k % S);
-    drain(s);
+    join_slot(s);
     const std::uint64_t poff = k * C;
     const std::uint64_t len = std::min<std::uint64_t>(C, r.in_len - poff);
     const bool last = k + 1 == npieces;
@@ -1132,11 +1150,10 @@ std::uint64_t file_shard(DevCtx& d, const Range& r, int in_fd, int out_fd, std::
     if (olen) PAES_CK(cudaMemcpyAsync(d.hbuf[s], d.dbuf[s], olen, cudaMemcpyDeviceToHost, d.st[s]));
     if (last && a.check_pad) PAES_CK(cudaMemcpyAsync(d.h_status, d.d_status, 4, cudaMemcpyDeviceToHost, d.st[s]));
     PAES_CK(cudaEventRecord(d.ev[s], d.st[s]));
-    pend_off[s] = static_cast<std::int64_t>(off + poff);
-    pend_len[s] = olen;
+    writer[s] = std::thread(write_slot, s, off + poff, olen);
     out_total = poff + olen;
   }
-  for (int s = 0; s < S; ++s) drain(s);
+  for (int s = 0; s < S; ++s) join_slot(s);
   if (r.check_pad) {
     const std::uint32_t k = *d.h_status;
     if (k == 0xffffffffu) throw PaddingError("unpad: invalid pad bytes");
