@@ -1,0 +1,65 @@
+"""Concurrent calls from many host threads (the reference runs encrypt_ecb
+from W threads at once, exec.cpp:153-175): every API path must stay
+bit-exact when its calls interleave.  ctypes releases the GIL, so the
+threads really run inside the library together."""
+import os
+import random
+from concurrent.futures import ThreadPoolExecutor
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def test_concurrent_mixed_calls(paes, gpu, orc):
+    import torch
+
+    rnd = random.Random(99)
+    jobs = []
+    for i in range(48):
+        kind = ["bytes", "ecb", "device", "batch", "pageable_big"][i % 5]
+        n = rnd.choice([0, 1, 17, 1000, 65536, 300_001, 3 << 20])
+        jobs.append((kind, n, os.urandom(16), os.urandom(n)))
+
+    def run(job):
+        kind, n, key, data = job
+        if kind == "bytes":
+            ct = paes.encrypt_bytes(data, key)
+            assert ct == orc.encrypt_chunk(data, True, key)
+            assert paes.decrypt_bytes(ct, key) == data
+        elif kind == "ecb":
+            d = data[: len(data) - len(data) % 16]
+            assert paes.encrypt_ecb(d, key) == orc.ecb(0, d, key)
+        elif kind == "device":
+            s = torch.cuda.Stream()
+            src = torch.frombuffer(bytearray(data + b"\0" * 16), dtype=torch.uint8).cuda()
+            dst = torch.zeros(len(data) + 32, dtype=torch.uint8, device="cuda")
+            torch.cuda.synchronize()
+            m = paes.chunk_device(0, src.data_ptr(), n, True, paes.round_keys(key), dst.data_ptr(), 0, s.cuda_stream)
+            s.synchronize()
+            assert dst[:m].cpu().numpy().tobytes() == orc.encrypt_chunk(data, True, key)
+        elif kind == "batch":
+            parts = [data[:n // 3], data[n // 3:]]
+            keys = [key, bytes(reversed(key))]
+            in_off = [0, (len(parts[0]) + 15) // 16 * 16]
+            total_in = in_off[1] + len(parts[1]) + 16
+            out_off = [0, (len(parts[0]) // 16 + 1) * 16]
+            total_out = out_off[1] + (len(parts[1]) // 16 + 1) * 16
+            hin = np.zeros(total_in, dtype=np.uint8)
+            hin[in_off[0]:in_off[0] + len(parts[0])] = np.frombuffer(parts[0], dtype=np.uint8)
+            hin[in_off[1]:in_off[1] + len(parts[1])] = np.frombuffer(parts[1], dtype=np.uint8)
+            hout = np.zeros(total_out, dtype=np.uint8)
+            rks = b"".join(paes.round_keys(k) for k in keys)
+            ol = paes.ecb_batch_host(0, hin.ctypes.data, hout.ctypes.data, in_off, out_off,
+                                     [len(p) for p in parts], rks, True)
+            for i in range(2):
+                assert hout[out_off[i]:out_off[i] + ol[i]].tobytes() == orc.encrypt_chunk(parts[i], True, keys[i])
+        else:  # pageable, several pieces through the staged ring
+            big = data * 4
+            assert paes.encrypt_bytes(big, key) == orc.encrypt_chunk(big, True, key, threads=2)
+        return kind
+
+    with ThreadPoolExecutor(12) as ex:
+        done = list(ex.map(run, jobs))
+    assert len(done) == len(jobs)
