@@ -16,8 +16,8 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB_DIR = os.path.join(PKG, "lib")
 LIB = os.path.join(LIB_DIR, "libpaes_cuda.so")
-SOURCES = ["aes_kernels.cu", "aes_bitsliced.cu", "paes_cuda.cu", "host_rules.cpp"]
-HEADERS = ["aes_kernels.cuh", "aes_tables.hpp", "host_rules.hpp", "launch.hpp", "sbox_bitsliced.inc"]
+SOURCES = ["aes_kernels.cu", "aes_bitsliced.cu", "runtime.cu", "abi_core.cu", "abi_batch.cu", "abi_file.cu", "host_rules.cpp"]
+HEADERS = ["aes_kernels.cuh", "aes_tables.hpp", "host_rules.hpp", "launch.hpp", "runtime.hpp", "sbox_bitsliced.inc"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 # system g++: links libstdc++ dynamically, like the torch/numpy in the same process

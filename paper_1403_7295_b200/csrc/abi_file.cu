@@ -1,0 +1,272 @@
+// abi_file.cu -- C ABI of the file path: run_job with the "gpu" strategy
+// (exec.hpp:18-51, exec.cpp:340-347): parallel pread -> pinned ring -> H2D /
+// kernel / D2H -> writer threads into a shared mapping of the temp file,
+// rename on success (AtomicOutput, exec.cpp:80-106).
+#include <fcntl.h>
+#include <sys/mman.h>
+#include <sys/stat.h>
+#include <unistd.h>
+
+#include <cerrno>
+#include <chrono>
+#include <sstream>
+#include <thread>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "runtime.hpp"
+
+using namespace paes_b200;
+using namespace paes_b200::rt;
+
+// ============================================================ file path
+namespace {
+
+struct Fd {
+  int fd = -1;
+  ~Fd() {
+    if (fd >= 0) ::close(fd);
+  }
+};
+
+struct IoFail {
+  std::string msg;
+};
+
+struct Map {
+  std::uint8_t* p = nullptr;
+  std::uint64_t n = 0;
+  ~Map() {
+    if (p) ::munmap(p, n);
+  }
+};
+
+void pread_all(int fd, std::uint8_t* p, std::uint64_t n, std::uint64_t off, const std::string& path) {
+  std::uint64_t got = 0;
+  while (got < n) {
+    const ssize_t r = ::pread(fd, p + got, n - got, static_cast<off_t>(off + got));
+    if (r < 0 && errno == EINTR) continue;
+    if (r <= 0) throw IoFail{"short read: " + path};
+    got += static_cast<std::uint64_t>(r);
+  }
+}
+
+void pwrite_all(int fd, const std::uint8_t* p, std::uint64_t n, std::uint64_t off, const std::string& path) {
+  std::uint64_t put = 0;
+  while (put < n) {
+    const ssize_t r = ::pwrite(fd, p + put, n - put, static_cast<off_t>(off + put));
+    if (r < 0 && errno == EINTR) continue;
+    if (r <= 0) throw IoFail{"write failed: " + path};
+    put += static_cast<std::uint64_t>(r);
+  }
+}
+
+// Split one pread/pwrite of a pinned slot across several host threads: a
+// single thread copying from/to the page cache runs at a few GB/s, far below
+// the PCIe rate the slot is DMA'd at.  Threads per shard = host threads /
+// shards, at most 8.
+unsigned g_io_threads_per_shard = 0;  // 0 = auto
+
+template <class F>
+void par_io(std::uint64_t n, unsigned threads, F&& f) {
+  constexpr std::uint64_t kGrain = 4ull << 20;
+  const std::uint64_t parts = std::min<std::uint64_t>(threads, (n + kGrain - 1) / kGrain);
+  if (parts <= 1) {
+    f(0, n);
+    return;
+  }
+  const std::uint64_t step = ((n / parts) + 4095) & ~std::uint64_t(4095);
+  std::vector<std::thread> pool;
+  std::vector<std::string> errs(parts);
+  for (std::uint64_t i = 1; i < parts; ++i) {
+    const std::uint64_t b = std::min(n, i * step), e = std::min(n, (i + 1) * step);
+    if (b >= e) break;
+    pool.emplace_back([&, i, b, e] {
+      try {
+        f(b, e - b);
+      } catch (const IoFail& x) {
+        errs[i] = x.msg;
+      }
+    });
+  }
+  try {
+    f(0, std::min(n, step));
+  } catch (const IoFail& x) {
+    errs[0] = x.msg;
+  }
+  for (auto& t : pool) t.join();
+  for (const auto& e : errs)
+    if (!e.empty()) throw IoFail{e};
+}
+
+// One GPU's shard of a file job: pread into pinned slots, H2D, kernel, D2H
+// back into the same slot, pwrite -- all slots in flight at once.  Returns
+// the output bytes written (decrypt final: unpadded).
+std::uint64_t file_shard(DevCtx& d, const Range& r, int in_fd, int out_fd, std::uint8_t* out_map, std::uint64_t off,
+                         const KeyWords& kw, const std::string& in_path, const std::string& out_path,
+                         unsigned io_threads) {
+  DeviceGuard g(d.id);
+  ensure_pipeline(d, true);
+  const int S = static_cast<int>(d.st.size());
+  const std::uint64_t C = piece_size(r.in_len, d.chunk, S);
+  const std::uint64_t npieces = std::max<std::uint64_t>(1, (r.in_len + C - 1) / C);
+  // Each slot's output is written back by its own writer thread (it waits on
+  // the slot's event, then copies into the output mapping), so writing piece
+  // k-1 overlaps reading piece k; a slot is refilled only after its writer
+  // has been joined.
+  std::vector<std::thread> writer(S);
+  std::vector<std::string> werr(S);
+  auto write_slot = [&](int s, std::uint64_t base, std::uint64_t len) {
+    try {
+      PAES_CK(cudaSetDevice(d.id));
+      PAES_CK(cudaEventSynchronize(d.ev[s]));
+      std::uint8_t* slot = d.hbuf[s];
+      if (out_map)  // page faults of a shared mapping proceed in parallel; pwrite serialises on the inode
+        par_io(len, io_threads, [&](std::uint64_t o, std::uint64_t n) { std::memcpy(out_map + base + o, slot + o, n); });
+      else
+        par_io(len, io_threads, [&](std::uint64_t o, std::uint64_t n) { pwrite_all(out_fd, slot + o, n, base + o, out_path); });
+    } catch (const IoFail& e) {
+      werr[s] = e.msg;
+    } catch (const CudaFail& e) {
+      werr[s] = e.msg;
+    }
+  };
+  auto join_slot = [&](int s) {
+    if (writer[s].joinable()) writer[s].join();
+    if (!werr[s].empty()) throw IoFail{werr[s]};
+  };
+  struct JoinAll {  // never leave a writer running on an exception
+    std::vector<std::thread>& w;
+    ~JoinAll() {
+      for (auto& t : w)
+        if (t.joinable()) t.join();
+    }
+  } join_all{writer};
+  std::uint64_t out_total = 0;
+  for (std::uint64_t k = 0; k < npieces; ++k) {
+    const int s = static_cast<int>(k % S);
+    join_slot(s);
+    const std::uint64_t poff = k * C;
+    const std::uint64_t len = std::min<std::uint64_t>(C, r.in_len - poff);
+    const bool last = k + 1 == npieces;
+    std::uint8_t* slot = d.hbuf[s];
+    par_io(len, io_threads,
+           [&](std::uint64_t o, std::uint64_t n) { pread_all(in_fd, slot + o, n, off + poff + o, in_path); });
+    EcbArgs a = make_args(r, d.dbuf[s], d.dbuf[s], len, last, kw, d.d_status);
+    if (len) PAES_CK(cudaMemcpyAsync(d.dbuf[s], d.hbuf[s], len, cudaMemcpyHostToDevice, d.st[s]));
+    if (a.check_pad) PAES_CK(cudaMemsetAsync(d.d_status, 0xff, 4, d.st[s]));
+    PAES_CK(launch_ecb(r.dec, a, d.sm_count, d.st[s]));
+    const std::uint64_t olen = a.nblocks * 16;
+    if (olen) PAES_CK(cudaMemcpyAsync(d.hbuf[s], d.dbuf[s], olen, cudaMemcpyDeviceToHost, d.st[s]));
+    if (last && a.check_pad) PAES_CK(cudaMemcpyAsync(d.h_status, d.d_status, 4, cudaMemcpyDeviceToHost, d.st[s]));
+    PAES_CK(cudaEventRecord(d.ev[s], d.st[s]));
+    writer[s] = std::thread(write_slot, s, off + poff, olen);
+    out_total = poff + olen;
+  }
+  for (int s = 0; s < S; ++s) join_slot(s);
+  if (r.check_pad) {
+    const std::uint32_t k = *d.h_status;
+    if (k == 0xffffffffu) throw PaddingError("unpad: invalid pad bytes");
+    out_total -= k;
+  }
+  return out_total;
+}
+
+}  // namespace
+
+extern "C" int paes_cuda_run_job(const char* input_path, const char* output_path, const uint8_t key[16],
+                                 uint32_t workers, int dir, paes_job_outcome* outcome) {
+  const auto t0 = std::chrono::steady_clock::now();
+  std::string tmp;
+  const int rc = guarded([&] {
+    if (!input_path || !output_path || !key) throw std::invalid_argument("null argument");
+    if (dir != PAES_ENCRYPT && dir != PAES_DECRYPT) throw std::invalid_argument("bad dir");
+    const bool dec = dir == PAES_DECRYPT;
+    const std::string in_path(input_path), out_path(output_path);
+    Fd in;
+    in.fd = ::open(input_path, O_RDONLY);
+    if (in.fd < 0) return fail(PAES_EIO, "cannot open input: " + in_path);
+    struct stat stt {};
+    if (::fstat(in.fd, &stt) != 0) return fail(PAES_EIO, "cannot stat input: " + in_path);
+    const std::uint64_t len = static_cast<std::uint64_t>(stt.st_size);
+    const auto devs = device_list(static_cast<int>(workers));
+    const auto plan = dec ? plan_decrypt_chunks(len, static_cast<unsigned>(devs.size()))
+                          : plan_chunks(len, static_cast<unsigned>(devs.size()));
+    std::uint8_t rk[176];
+    expand_key(key, rk);
+    const KeyWords kw = dec ? dec_key_words(rk) : enc_key_words(rk);
+    tmp = out_path + ".part." + std::to_string(::getpid());
+    Fd out;
+    out.fd = ::open(tmp.c_str(), O_RDWR | O_CREAT | O_TRUNC, 0644);
+    if (out.fd < 0) return fail(PAES_EIO, "cannot open output: " + tmp);
+    // Output through a shared mapping sized to the worst case (trimmed after
+    // a decrypt's unpad); plain pwrite if the file system refuses mmap.
+    const std::uint64_t cap = dec ? len : (len / 16 + 1) * 16;
+    Map map;
+    if (cap && ::ftruncate(out.fd, static_cast<off_t>(cap)) == 0) {
+      void* p = ::mmap(nullptr, cap, PROT_READ | PROT_WRITE, MAP_SHARED, out.fd, 0);
+      if (p != MAP_FAILED) {
+        map.p = static_cast<std::uint8_t*>(p);
+        map.n = cap;
+      }
+    }
+    std::vector<std::uint64_t> produced(plan.size(), 0);
+    std::vector<std::string> failures(plan.size());
+    auto work = [&](std::size_t i) {
+      const Chunk& c = plan[i];
+      Range r;
+      r.dec = dec;
+      r.in_len = c.raw_len;
+      r.pad = !dec && c.is_final;
+      r.check_pad = dec && c.is_final;
+      try {
+        DevCtx& d = device(devs[i]);
+        std::lock_guard<std::mutex> lk(d.mu);
+        const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+        const unsigned io = g_io_threads_per_shard
+                                ? g_io_threads_per_shard
+                                : std::clamp<unsigned>(hw / static_cast<unsigned>(plan.size()), 1u, 8u);
+        produced[i] = file_shard(d, r, in.fd, out.fd, map.p, c.offset, kw, in_path, tmp, io);
+      } catch (const CudaFail& e) {
+        failures[i] = e.msg;
+      } catch (const IoFail& e) {
+        failures[i] = e.msg;
+      } catch (const std::exception& e) {
+        failures[i] = e.what();
+      }
+    };
+    if (plan.size() == 1) {
+      work(0);
+    } else {
+      std::vector<std::thread> pool;
+      for (std::size_t i = 0; i < plan.size(); ++i) pool.emplace_back(work, i);
+      for (auto& t : pool) t.join();
+    }
+    std::ostringstream failed;
+    bool any = false;
+    for (std::size_t i = 0; i < failures.size(); ++i) {
+      if (failures[i].empty()) continue;
+      failed << (any ? "; " : "") << "chunk " << i << ": " << failures[i];
+      any = true;
+    }
+    if (any) return fail(PAES_EWORKER, "worker failure: " + failed.str());
+    std::uint64_t total = 0;
+    for (auto p : produced) total += p;
+    if (::ftruncate(out.fd, static_cast<off_t>(total)) != 0) return fail(PAES_EIO, "truncate failed: " + tmp);
+    if (::rename(tmp.c_str(), output_path) != 0) return fail(PAES_EIO, "rename failed: " + out_path);
+    tmp.clear();
+    if (outcome) {
+      outcome->bytes_in = len;
+      outcome->bytes_out = total;
+      outcome->seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    }
+    return PAES_OK;
+  });
+  if (rc != PAES_OK && !tmp.empty()) ::unlink(tmp.c_str());  // no partial output (exec.cpp:86-91)
+  return rc;
+}

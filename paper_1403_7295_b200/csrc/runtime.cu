@@ -1,0 +1,374 @@
+// runtime.cu -- the host runtime behind the C ABI: per-device contexts, the
+// multi-stream host<->device ring (zero-copy small path, pinned direct ring,
+// staged ring for pageable memory) and the multi-GPU block-range sharder.
+//
+// Reference boundary: aes::encrypt_ecb/decrypt_ecb
+// (aes.hpp:86-89), paes::encrypt_chunk/decrypt_chunk (exec.hpp:61-65) and
+// run_job's strategy dispatch (exec.cpp:340-347).  Exceptions become codes:
+// std::invalid_argument -> PAES_EINVAL, PaddingError -> PAES_EBADMSG,
+// IoError -> PAES_EIO, WorkerError -> PAES_EWORKER, CUDA -> PAES_ECUDA.
+#include <cuda_runtime.h>
+#include <fcntl.h>
+#include <sys/mman.h>
+#include <sys/stat.h>
+#include <unistd.h>
+
+#include <algorithm>
+#include <cerrno>
+#include <chrono>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <sstream>
+#include <string>
+#include <thread>
+#include <vector>
+#include "runtime.hpp"
+
+namespace paes_b200::rt {
+
+thread_local std::string t_err;
+
+int fail(int code, const std::string& msg) {
+  t_err = msg;
+  return code;
+}
+
+
+DevCtx g_dev[kMaxDev];
+std::mutex g_cfg_mu;
+std::vector<int> g_devices;  // empty = all visible
+std::uint64_t g_chunk = 64ull << 20;  // scripts/pcie_probe.py: 64-128 MiB pieces reach ~94% of concurrent H2D+D2H
+int g_streams = 3;
+
+int visible_devices() {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
+
+// Lazily initialise a device: kernel attributes, status words.
+DevCtx& device(int id) {
+  const int n = visible_devices();
+  if (id < 0 || id >= n || id >= kMaxDev)
+    throw CudaFail{PAES_ENODEV, "no such CUDA device: " + std::to_string(id) + " (visible: " + std::to_string(n) + ")"};
+  DevCtx& d = g_dev[id];
+  std::lock_guard<std::mutex> lk(d.mu);
+  if (!d.ready) {
+    DeviceGuard g(id);
+    PAES_CK(cudaDeviceGetAttribute(&d.sm_count, cudaDevAttrMultiProcessorCount, id));
+    PAES_CK(prepare_kernels());
+    PAES_CK(cudaMalloc(&d.d_status, 4096));
+    PAES_CK(cudaMallocHost(&d.h_status, 4096));
+    PAES_CK(cudaMalloc(&d.d_acc, 64));
+    PAES_CK(cudaMallocHost(&d.h_acc, 64));
+    d.id = id;
+    d.ready = true;
+  }
+  return d;
+}
+
+// Pipeline buffers (device rings + optional pinned host ring); d.mu held.
+void ensure_pipeline(DevCtx& d, bool need_host) {
+  std::uint64_t chunk;
+  int ns;
+  {
+    std::lock_guard<std::mutex> lk(g_cfg_mu);
+    chunk = g_chunk;
+    ns = g_streams;
+  }
+  if (d.chunk != chunk || static_cast<int>(d.st.size()) != ns) {
+    for (auto p : d.dbuf) cudaFree(p);
+    for (auto p : d.hbuf) cudaFreeHost(p);
+    for (auto s : d.st) cudaStreamDestroy(s);
+    for (auto e : d.ev) cudaEventDestroy(e);
+    d.dbuf.clear();
+    d.hbuf.clear();
+    d.st.clear();
+    d.ev.clear();
+    d.chunk = chunk;
+    for (int i = 0; i < ns; ++i) {
+      cudaStream_t s;
+      PAES_CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+      d.st.push_back(s);
+      cudaEvent_t e;
+      PAES_CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      d.ev.push_back(e);
+      std::uint8_t* p = nullptr;
+      PAES_CK(cudaMalloc(&p, chunk + 16));
+      d.dbuf.push_back(p);
+    }
+  }
+  if (need_host && d.hbuf.empty()) {
+    for (int i = 0; i < ns; ++i) {
+      std::uint8_t* p = nullptr;
+      PAES_CK(cudaMallocHost(&p, d.chunk + 16));
+      d.hbuf.push_back(p);
+    }
+  }
+}
+
+std::vector<int> device_list(int ngpus) {
+  std::vector<int> list;
+  {
+    std::lock_guard<std::mutex> lk(g_cfg_mu);
+    list = g_devices;
+  }
+  if (list.empty()) {
+    const int n = visible_devices();
+    for (int i = 0; i < n; ++i) list.push_back(i);
+  }
+  if (list.empty()) throw CudaFail{PAES_ENODEV, "no CUDA device visible"};
+  if (ngpus < 0) throw std::invalid_argument("ngpus must be >= 0");
+  if (ngpus > 0) {
+    if (ngpus > static_cast<int>(list.size()))
+      throw CudaFail{PAES_ENODEV, "requested " + std::to_string(ngpus) + " GPUs, " + std::to_string(list.size()) +
+                                      " available"};
+    list.resize(ngpus);
+  }
+  return list;
+}
+
+EcbArgs make_args(const Range& r, const std::uint8_t* in, std::uint8_t* out, std::uint64_t in_len, bool last,
+                  const KeyWords& kw, std::uint32_t* status) {
+  EcbArgs a{};
+  a.in = in;
+  a.out = out;
+  a.nfull = in_len / 16;
+  a.tail_len = static_cast<std::uint32_t>(in_len % 16);
+  a.nblocks = a.nfull + ((r.pad && last) ? 1 : 0);
+  a.check_pad = (r.check_pad && last) ? 1u : 0u;
+  a.status = status;
+  a.k = kw;
+  return a;
+}
+
+// Piece size for a range: the staging chunk, but small enough that even a
+// short range is split into ~2 pieces per stream so copy-in, kernel and
+// copy-out still overlap (a single 64 MiB piece would serialise them).
+std::uint64_t piece_size(std::uint64_t len, std::uint64_t chunk, int streams) {
+  const std::uint64_t floor_piece = std::min<std::uint64_t>(4ull << 20, chunk);
+  const std::uint64_t p = (len / (2ull * static_cast<std::uint64_t>(streams)) + 15) & ~std::uint64_t(15);
+  return std::clamp(p, floor_piece, chunk);
+}
+
+// Host range on one device through the stream ring (d.mu held).  Returns the
+// number of output bytes (decrypt+check: unpadded).
+// Small host ranges (<= kSmallBytes): one memcpy into a mapped pinned buffer,
+// ONE kernel that reads and writes that host buffer over PCIe (zero-copy),
+// one sync, one memcpy out.  Replaces H2D + launch + D2H (three commands and
+// their latencies) for the short messages of config 3 / encrypt_bytes.
+constexpr std::uint64_t kSmallBytes = 1ull << 20;
+
+struct SmallBuf {
+  std::uint8_t* host = nullptr;  // mapped pinned, kSmallBytes + 32
+  std::uint8_t* dev = nullptr;   // its device alias
+  std::uint32_t* status_host = nullptr;
+  std::uint32_t* status_dev = nullptr;
+};
+SmallBuf g_small[kMaxDev];
+
+std::uint64_t run_small(DevCtx& d, const Range& r, const std::uint8_t* in, std::uint8_t* out, const KeyWords& kw) {
+  SmallBuf& sb = g_small[d.id];
+  if (!sb.host) {
+    void* p = nullptr;
+    PAES_CK(cudaHostAlloc(&p, kSmallBytes + 4096, cudaHostAllocMapped | cudaHostAllocPortable));
+    sb.host = static_cast<std::uint8_t*>(p);
+    PAES_CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&sb.dev), p, 0));
+    sb.status_host = reinterpret_cast<std::uint32_t*>(sb.host + kSmallBytes + 2048);
+    sb.status_dev = reinterpret_cast<std::uint32_t*>(sb.dev + kSmallBytes + 2048);
+  }
+  if (r.in_len) std::memcpy(sb.host, in, r.in_len);
+  *sb.status_host = 0xffffffffu;  // sentinel: unchecked => PaddingError
+  EcbArgs a = make_args(r, sb.dev, sb.dev, r.in_len, true, kw, sb.status_dev);
+  PAES_CK(launch_ecb(r.dec, a, d.sm_count, d.st[0]));
+  PAES_CK(cudaStreamSynchronize(d.st[0]));
+  std::uint64_t olen = a.nblocks * 16;
+  if (olen) std::memcpy(out, sb.host, olen);
+  if (r.check_pad) {
+    const std::uint32_t k = *reinterpret_cast<volatile std::uint32_t*>(sb.status_host);
+    if (k == 0xffffffffu) throw PaddingError("unpad: invalid pad bytes");
+    olen -= k;
+  }
+  return olen;
+}
+
+bool is_pinned(const void* p) {
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost;
+}
+
+// memcpy split over host threads (a single core moves ~10 GB/s; the pinned
+// slots are fed at PCIe rate).
+void par_copy(std::uint8_t* dst, const std::uint8_t* src, std::uint64_t n) {
+  constexpr std::uint64_t kGrain = 8ull << 20;
+  const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+  const std::uint64_t parts = std::min<std::uint64_t>(std::min(hw, 8u), (n + kGrain - 1) / kGrain);
+  if (parts <= 1) {
+    if (n) std::memcpy(dst, src, n);
+    return;
+  }
+  const std::uint64_t step = ((n / parts) + 4095) & ~std::uint64_t(4095);
+  std::vector<std::thread> pool;
+  for (std::uint64_t i = 1; i < parts; ++i) {
+    const std::uint64_t b = std::min(n, i * step), e = std::min(n, (i + 1) * step);
+    if (b < e) pool.emplace_back([=] { std::memcpy(dst + b, src + b, e - b); });
+  }
+  std::memcpy(dst, src, std::min(n, step));
+  for (auto& t : pool) t.join();
+}
+
+// Pageable host buffers (std::vector, Python bytes): stage through the pinned
+// slot ring ourselves -- copy piece k in while the GPU works on earlier
+// pieces, copy each finished piece out when its slot comes round again.  The
+// driver's own staging of pageable cudaMemcpyAsync serialises at ~7 GB/s.
+std::uint64_t run_host_range_staged(DevCtx& d, const Range& r, const std::uint8_t* in, std::uint8_t* out,
+                                    const KeyWords& kw) {
+  ensure_pipeline(d, true);
+  const int S = static_cast<int>(d.st.size());
+  const std::uint64_t C = piece_size(r.in_len, d.chunk, S);
+  const std::uint64_t npieces = std::max<std::uint64_t>(1, (r.in_len + C - 1) / C);
+  std::vector<std::int64_t> pend_off(S, -1);
+  std::vector<std::uint64_t> pend_len(S, 0);
+  auto drain = [&](int s) {
+    if (pend_off[s] < 0) return;
+    PAES_CK(cudaEventSynchronize(d.ev[s]));
+    par_copy(out + pend_off[s], d.hbuf[s], pend_len[s]);
+    pend_off[s] = -1;
+  };
+  std::uint64_t out_total = 0;
+  for (std::uint64_t k = 0; k < npieces; ++k) {
+    const int s = static_cast<int>(k % S);
+    drain(s);
+    const std::uint64_t off = k * C;
+    const std::uint64_t len = std::min<std::uint64_t>(C, r.in_len - off);
+    const bool last = k + 1 == npieces;
+    par_copy(d.hbuf[s], in + off, len);
+    EcbArgs a = make_args(r, d.dbuf[s], d.dbuf[s], len, last, kw, d.d_status);
+    if (len) PAES_CK(cudaMemcpyAsync(d.dbuf[s], d.hbuf[s], len, cudaMemcpyHostToDevice, d.st[s]));
+    if (a.check_pad) PAES_CK(cudaMemsetAsync(d.d_status, 0xff, 4, d.st[s]));
+    PAES_CK(launch_ecb(r.dec, a, d.sm_count, d.st[s]));
+    const std::uint64_t olen = a.nblocks * 16;
+    if (olen) PAES_CK(cudaMemcpyAsync(d.hbuf[s], d.dbuf[s], olen, cudaMemcpyDeviceToHost, d.st[s]));
+    if (last && a.check_pad) PAES_CK(cudaMemcpyAsync(d.h_status, d.d_status, 4, cudaMemcpyDeviceToHost, d.st[s]));
+    PAES_CK(cudaEventRecord(d.ev[s], d.st[s]));
+    pend_off[s] = static_cast<std::int64_t>(off);
+    pend_len[s] = olen;
+    out_total = off + olen;
+  }
+  for (int s = 0; s < S; ++s) drain(s);
+  if (r.check_pad) {
+    const std::uint32_t k = *d.h_status;
+    if (k == 0xffffffffu) throw PaddingError("unpad: invalid pad bytes");
+    out_total -= k;
+  }
+  return out_total;
+}
+
+std::uint64_t run_host_range(DevCtx& d, const Range& r, const std::uint8_t* in, std::uint8_t* out, const KeyWords& kw) {
+  DeviceGuard g(d.id);
+  ensure_pipeline(d, false);
+  if (r.in_len <= std::min(kSmallBytes, d.chunk)) return run_small(d, r, in, out, kw);
+  if (!is_pinned(in) || !is_pinned(out)) return run_host_range_staged(d, r, in, out, kw);
+  const int S = static_cast<int>(d.st.size());
+  const std::uint64_t C = piece_size(r.in_len, d.chunk, S);
+  const std::uint64_t npieces = std::max<std::uint64_t>(1, (r.in_len + C - 1) / C);
+  std::uint64_t out_total = 0;
+  for (std::uint64_t k = 0; k < npieces; ++k) {
+    const int s = static_cast<int>(k % S);
+    const std::uint64_t off = k * C;
+    const std::uint64_t len = std::min<std::uint64_t>(C, r.in_len - off);
+    const bool last = k + 1 == npieces;
+    EcbArgs a = make_args(r, d.dbuf[s], d.dbuf[s], len, last, kw, d.d_status);
+    if (len) PAES_CK(cudaMemcpyAsync(d.dbuf[s], in + off, len, cudaMemcpyHostToDevice, d.st[s]));
+    if (a.check_pad) PAES_CK(cudaMemsetAsync(d.d_status, 0xff, 4, d.st[s]));  // sentinel: unchecked => PaddingError
+    PAES_CK(launch_ecb(r.dec, a, d.sm_count, d.st[s]));
+    const std::uint64_t olen = a.nblocks * 16;
+    if (olen) PAES_CK(cudaMemcpyAsync(out + off, d.dbuf[s], olen, cudaMemcpyDeviceToHost, d.st[s]));
+    if (last && a.check_pad)
+      PAES_CK(cudaMemcpyAsync(d.h_status, d.d_status, 4, cudaMemcpyDeviceToHost, d.st[s]));
+    out_total = off + olen;
+  }
+  for (auto s : d.st) PAES_CK(cudaStreamSynchronize(s));
+  if (r.check_pad) {
+    const std::uint32_t k = *d.h_status;
+    if (k == 0xffffffffu) throw PaddingError("unpad: invalid pad bytes");
+    out_total -= k;
+  }
+  return out_total;
+}
+
+// Shard a host buffer over devices with the plan_chunks rule (encrypt) or
+// plan_decrypt_chunks (decrypt); output offsets equal input offsets.
+int host_transform(int dir, const std::uint8_t* in, std::uint64_t len, bool is_final, const std::uint8_t* rk,
+                   std::uint8_t* out, std::uint64_t* out_len, int ngpus) {
+  if (dir != PAES_ENCRYPT && dir != PAES_DECRYPT) throw std::invalid_argument("dir must be 0 (encrypt) or 1 (decrypt)");
+  if (!rk) throw std::invalid_argument("null round keys");
+  const bool dec = dir == PAES_DECRYPT;
+  if (!is_final && len % 16 != 0) throw std::invalid_argument("non-final chunk length must be a multiple of 16");
+  if (dec && len % 16 != 0) throw std::invalid_argument("decrypt: length must be a multiple of 16");
+  if (len && !in) throw std::invalid_argument("null input");
+  if (dec && is_final && len == 0) throw PaddingError("unpad: length must be a non-zero multiple of 16");
+  if (len == 0 && !(is_final && !dec)) {
+    if (out_len) *out_len = 0;
+    return PAES_OK;
+  }
+  if (!out) throw std::invalid_argument("null output");
+  const auto devs = device_list(ngpus);
+  const KeyWords kw = dec ? dec_key_words(rk) : enc_key_words(rk);
+  const auto plan = dec ? plan_decrypt_chunks(len, static_cast<unsigned>(devs.size()))
+                        : plan_chunks(len, static_cast<unsigned>(devs.size()));
+  std::vector<std::uint64_t> produced(plan.size(), 0);
+  std::vector<int> codes(plan.size(), PAES_OK);
+  std::vector<std::string> msgs(plan.size());
+  auto work = [&](std::size_t i) {
+    const Chunk& c = plan[i];
+    Range r;
+    r.dec = dec;
+    r.in_len = c.raw_len;
+    r.pad = !dec && is_final && c.is_final;
+    r.check_pad = dec && is_final && c.is_final;
+    codes[i] = guarded([&] {
+      DevCtx& d = device(devs[i]);
+      std::lock_guard<std::mutex> lk(d.mu);
+      produced[i] = run_host_range(d, r, in + c.offset, out + c.offset, kw);
+      return PAES_OK;
+    });
+    if (codes[i]) msgs[i] = t_err;
+  };
+  if (plan.size() == 1) {
+    work(0);
+  } else {
+    std::vector<std::thread> pool;
+    for (std::size_t i = 0; i < plan.size(); ++i) pool.emplace_back(work, i);
+    for (auto& t : pool) t.join();
+  }
+  for (std::size_t i = 0; i < plan.size(); ++i)
+    if (codes[i]) return fail(codes[i], msgs[i]);
+  std::uint64_t total = 0;
+  for (auto p : produced) total += p;
+  if (out_len) *out_len = total;
+  return PAES_OK;
+}
+
+
+void set_device_list(const std::vector<int>& ids) {
+  std::lock_guard<std::mutex> lk(g_cfg_mu);
+  g_devices = ids;
+}
+
+void set_pipeline_config(std::uint64_t chunk_bytes, int streams) {
+  std::lock_guard<std::mutex> lk(g_cfg_mu);
+  if (chunk_bytes) g_chunk = chunk_bytes;
+  if (streams) g_streams = streams;
+}
+
+}  // namespace paes_b200::rt

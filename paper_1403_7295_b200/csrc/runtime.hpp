@@ -1,0 +1,116 @@
+// runtime.hpp -- internal runtime shared by the C-ABI translation units:
+// error mapping (C++ exceptions -> PAES_* codes), per-device contexts, the
+// device list / pipeline configuration and the host<->device stream ring.
+// Not installed; the public boundary is include/paes_cuda.h.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/paes_cuda.h"
+#include "host_rules.hpp"
+#include "launch.hpp"
+
+namespace paes_b200::rt {
+
+extern thread_local std::string t_err;
+int fail(int code, const std::string& msg);
+
+struct CudaFail {
+  int code;
+  std::string msg;
+};
+
+#define PAES_CK(call)                                                                           \
+  do {                                                                                          \
+    const cudaError_t e_ = (call);                                                              \
+    if (e_ != cudaSuccess) throw CudaFail{PAES_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e_)}; \
+  } while (0)
+
+// Runs `f`, mapping C++ exceptions to C-ABI codes (no exception crosses the ABI).
+template <class F>
+int guarded(F&& f) {
+  try {
+    return f();
+  } catch (const CudaFail& e) {
+    return fail(e.code, e.msg);
+  } catch (const PaddingError& e) {
+    return fail(PAES_EBADMSG, e.what());
+  } catch (const std::invalid_argument& e) {
+    return fail(PAES_EINVAL, e.what());
+  } catch (const std::bad_alloc&) {
+    return fail(PAES_ECUDA, "host allocation failed");
+  } catch (const std::exception& e) {
+    return fail(PAES_ECUDA, e.what());
+  }
+}
+
+class DeviceGuard {
+ public:
+  explicit DeviceGuard(int dev) {
+    if (cudaGetDevice(&prev_) != cudaSuccess) prev_ = -1;
+    if (prev_ != dev) PAES_CK(cudaSetDevice(dev));
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    if (prev_ >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev_) cudaSetDevice(prev_);
+  }
+
+ private:
+  int prev_ = -1;
+};
+
+// ------------------------------------------------------------ device context
+struct DevCtx {
+  int id = -1;
+  bool ready = false;
+  int sm_count = 0;
+  std::mutex mu;  // serialises host-pointer pipelines / status words on this device
+  std::vector<cudaStream_t> st;
+  std::vector<std::uint8_t*> dbuf;  // chunk + 16 bytes each
+  std::vector<std::uint8_t*> hbuf;  // pinned staging for the file path
+  std::vector<cudaEvent_t> ev;
+  std::uint64_t chunk = 0;
+  std::uint32_t* d_status = nullptr;
+  std::uint32_t* h_status = nullptr;  // pinned
+  unsigned long long* d_acc = nullptr;
+  unsigned long long* h_acc = nullptr;  // pinned
+};
+
+constexpr int kMaxDev = 64;
+
+int visible_devices();
+// Lazily initialised context of device `id` (throws CudaFail ENODEV).
+DevCtx& device(int id);
+// Pipeline buffers (device ring, optional pinned host ring); d.mu held.
+void ensure_pipeline(DevCtx& d, bool need_host);
+// The devices host-pointer calls shard over (first `ngpus`, 0 = all).
+std::vector<int> device_list(int ngpus);
+void set_device_list(const std::vector<int>& ids);
+void set_pipeline_config(std::uint64_t chunk_bytes, int streams);
+
+// ------------------------------------------------------------ pieces
+// A transform over one contiguous range: whole input blocks, plus (encrypt,
+// final) the always-pad block built from `tail` trailing bytes, plus
+// (decrypt, final) a trailer check on the last block.
+struct Range {
+  bool dec = false;
+  bool pad = false;        // encrypt: append the PKCS#7 block
+  bool check_pad = false;  // decrypt: validate the trailer
+  std::uint64_t in_len = 0;
+};
+
+EcbArgs make_args(const Range& r, const std::uint8_t* in, std::uint8_t* out, std::uint64_t in_len, bool last,
+                  const KeyWords& kw, std::uint32_t* status);
+std::uint64_t piece_size(std::uint64_t len, std::uint64_t chunk, int streams);
+void par_copy(std::uint8_t* dst, const std::uint8_t* src, std::uint64_t n);
+// Host buffers on the device list: plan_chunks shards, one thread per shard.
+int host_transform(int dir, const std::uint8_t* in, std::uint64_t len, bool is_final, const std::uint8_t* rk,
+                   std::uint8_t* out, std::uint64_t* out_len, int ngpus);
+
+}  // namespace paes_b200::rt
