@@ -128,6 +128,9 @@ def main() -> None:
         ro.append({"in": s, "out": _paes.reject_outliers(s)})
     g["reject_outliers"] = ro
 
+    # the bench report's CSV contract (report.hpp:12-13)
+    g["csv_header"] = _paes.csv_header()
+
     with open(OUT, "w") as f:
         json.dump(g, f, indent=0, sort_keys=True)
     print("wrote", OUT, os.path.getsize(OUT), "bytes")
