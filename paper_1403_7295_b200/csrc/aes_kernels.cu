@@ -27,11 +27,17 @@ constexpr int kThreads = PAES_THREADS;  // one persistent CTA per SM (smem-limit
 // word index w:  region = w >> 14, row x = (w >> 6) & 255, table-in-region
 // t = (w >> 5) & 1, lane = w & 31.  Four consecutive words (4 lanes) share a
 // value, so the fill is one 16-byte store per 4 words.
+// The trip count is a compile-time constant (kernels launch with kThreads), so
+// the loop unrolls and all of a thread's table reads are in flight together
+// instead of one L2 round trip per 16-byte store.
 template <bool DEC>
 __device__ __forceinline__ void stage_tables(std::uint32_t* sm) {
   const std::uint32_t* base = DEC ? g_tab.td0 : g_tab.te0;
   constexpr int nvec = (DEC ? kDecSmemBytes : kEncSmemBytes) / 16;
-  for (int i = threadIdx.x; i < nvec; i += blockDim.x) {
+  static_assert(nvec % kThreads == 0, "staging assumes whole passes");
+#pragma unroll
+  for (int it = 0; it < nvec / kThreads; ++it) {
+    const int i = it * kThreads + static_cast<int>(threadIdx.x);
     const int w = i * 4;
     const int region = w >> 14;
     const int x = (w >> 6) & 255;
@@ -209,12 +215,26 @@ __global__ void __launch_bounds__(kThreads, 1) ecb_kernel(const __grid_constant_
   unsigned long long tile = blockIdx.x * wpc + threadIdx.x / 32;
   const unsigned long long tstride = gridDim.x * wpc;
 
-  // steady state: whole tiles of whole input blocks, no per-block checks
+  // steady state: whole tiles of whole input blocks, no per-block checks.
+  // The next tile's blocks are loaded before the current tile is computed
+  // (register double buffer), so a warp never waits on HBM at a tile start --
+  // otherwise the SM's warps, which advance in near lockstep on short
+  // launches, all stall on the same load latency together.
+  Block4 nxt[NB];
+  if (tile < full_tiles) {
+#pragma unroll
+    for (int j = 0; j < NB; ++j) nxt[j] = load_block<ALIGNED>(a.in + 16ull * (tile * kTile + lane + 32ull * j));
+  }
   for (; tile < full_tiles; tile += tstride) {
     const unsigned long long b0 = tile * kTile + lane;
     Block4 s[NB];
 #pragma unroll
-    for (int j = 0; j < NB; ++j) s[j] = load_block<ALIGNED>(a.in + 16ull * (b0 + 32ull * j));
+    for (int j = 0; j < NB; ++j) s[j] = nxt[j];
+    const unsigned long long next = tile + tstride;
+    if (next < full_tiles) {
+#pragma unroll
+      for (int j = 0; j < NB; ++j) nxt[j] = load_block<ALIGNED>(a.in + 16ull * (next * kTile + lane + 32ull * j));
+    }
     cipher<DEC, NB>(s, a.k.w, smb, lane4);
 #pragma unroll
     for (int j = 0; j < NB; ++j) store_block<ALIGNED>(a.out + 16ull * (b0 + 32ull * j), s[j]);
