@@ -234,6 +234,8 @@ class RefLib:
         L.ref_physical_cores.restype = C.c_uint
         L.ref_run_job.argtypes = [C.c_char_p, C.c_char_p, u8p, C.c_uint, C.c_int, C.c_int,
                                   C.POINTER(u64), C.POINTER(u64), C.POINTER(C.c_double)]
+        L.ref_run_job_ex.argtypes = [C.c_char_p, C.c_char_p, u8p, C.c_uint, C.c_int, C.c_int, C.c_char_p,
+                                     C.POINTER(u64), C.POINTER(u64), C.POINTER(C.c_double)]
 
     @staticmethod
     def _k(key: bytes):
@@ -315,6 +317,15 @@ class RefLib:
         if rc:
             raise ValueError("no samples")
         return list(out[: m.value])
+
+    def run_job(self, in_path: str, out_path: str, key: bytes, workers: int, strategy: int, direction: int,
+                worker_exe: str = ""):
+        """paes::run_job (strategy 0 sequential, 1 threads, 2 processes); returns
+        (rc, bytes_in, bytes_out, seconds)."""
+        bi, bo, sec = C.c_uint64(), C.c_uint64(), C.c_double()
+        rc = self.L.ref_run_job_ex(in_path.encode(), out_path.encode(), self._k(key), workers, strategy, direction,
+                                   worker_exe.encode(), C.byref(bi), C.byref(bo), C.byref(sec))
+        return rc, bi.value, bo.value, sec.value
 
     def cores(self):
         return int(self.L.ref_physical_cores()), int(self.L.ref_logical_cores())

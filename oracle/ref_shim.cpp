@@ -225,3 +225,31 @@ int ref_run_job(const char* in_path, const char* out_path, const std::uint8_t* k
 }
 
 }  // extern "C"
+
+extern "C" {
+
+// run_job with any strategy (2 = ProcessIsolated, whose workers are spawned
+// from `worker_exe`; exec.cpp:272-338) -- used to drive the GPU worker
+// (paper_1403_7295_b200/lib/paes_gpu_worker) from the reference's own,
+// unmodified process strategy.
+int ref_run_job_ex(const char* in_path, const char* out_path, const std::uint8_t* key, unsigned workers, int strategy,
+                   int dir, const char* worker_exe, std::uint64_t* bytes_in, std::uint64_t* bytes_out, double* seconds) {
+  return guarded([&] {
+    paes::JobSpec job;
+    job.input_path = in_path;
+    job.output_path = out_path;
+    job.key = to_key(key);
+    job.workers = workers;
+    job.strategy = strategy == 2   ? paes::ExecStrategy::ProcessIsolated
+                   : strategy == 1 ? paes::ExecStrategy::Threaded
+                                   : paes::ExecStrategy::Sequential;
+    job.direction = dir == 0 ? paes::Direction::Encrypt : paes::Direction::Decrypt;
+    if (worker_exe && *worker_exe) job.worker_exe = worker_exe;
+    const auto o = paes::run_job(job);
+    *bytes_in = o.bytes_in;
+    *bytes_out = o.bytes_out;
+    *seconds = o.seconds;
+  });
+}
+
+}  // extern "C"

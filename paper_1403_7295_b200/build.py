@@ -17,7 +17,8 @@ CSRC = os.path.join(PKG, "csrc")
 LIB_DIR = os.path.join(PKG, "lib")
 LIB = os.path.join(LIB_DIR, "libpaes_cuda.so")
 SOURCES = ["aes_kernels.cu", "aes_bitsliced.cu", "runtime.cu", "abi_core.cu", "abi_batch.cu", "abi_file.cu", "host_rules.cpp"]
-HEADERS = ["aes_kernels.cuh", "aes_tables.hpp", "host_rules.hpp", "launch.hpp", "runtime.hpp", "sbox_bitsliced.inc"]
+HEADERS = ["aes_kernels.cuh", "aes_tables.hpp", "host_rules.hpp", "launch.hpp", "runtime.hpp", "sbox_bitsliced.inc",
+           "gpu_worker.cpp"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 # system g++: links libstdc++ dynamically, like the torch/numpy in the same process
@@ -66,7 +67,25 @@ def build(force: bool = False, verbose: bool = False, defines=(), out_lib: str |
     os.replace(tmp, lib)
     for o in objs:
         os.unlink(o)
+    if out_lib is None:
+        build_worker()
     return lib
+
+
+WORKER = os.path.join(LIB_DIR, "paes_gpu_worker")
+
+
+def build_worker() -> str:
+    """The reference-protocol GPU worker executable (csrc/gpu_worker.cpp)."""
+    cxx = "/usr/bin/g++" if os.path.exists("/usr/bin/g++") else "g++"
+    cmd = [cxx, "-std=c++17", "-O2", "-Wall", "-Wextra", f"-I{os.path.join(ROOT, 'include')}",
+           os.path.join(CSRC, "gpu_worker.cpp"), "-o", WORKER + ".tmp", f"-L{LIB_DIR}", "-lpaes_cuda",
+           "-Wl,-rpath,$ORIGIN"]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError("worker build failed:\n%s%s" % (r.stdout, r.stderr))
+    os.replace(WORKER + ".tmp", WORKER)
+    return WORKER
 
 
 if __name__ == "__main__":

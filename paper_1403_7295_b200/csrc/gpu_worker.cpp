@@ -1,0 +1,134 @@
+// gpu_worker.cpp -- a GPU worker that speaks the reference's hidden worker
+// protocol.
+//
+//   paes_gpu_worker __worker --in P --offset N --len N --final 0|1
+//                   --dir encrypt|decrypt --keyfd FD --out P [--device D]
+//
+// Same arguments, key-over-inherited-pipe convention and exit codes as the
+// reference CLI's worker mode (paes_main.cpp:121-152 -> run_worker_chunk,
+// exec.cpp:349-373), so the reference's UNMODIFIED process strategy
+// (run_process_isolated, exec.cpp:272-338) drives B200s when its
+// JobSpec::worker_exe points here: one process per chunk, one GPU each.
+// The chunk is transformed by the library's host-pointer path
+// (paes_cuda_chunk).  Device: --device, else PAES_WORKER_DEVICE, else the
+// chunk's index (offset / len) modulo the visible devices.
+//
+// Exit codes (paes_main.cpp:316-325): 0 ok, 2 invalid argument, 1 anything else.
+#include <fcntl.h>
+#include <unistd.h>
+
+#include <cerrno>
+#include <cstdint>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "paes_cuda.h"
+
+namespace {
+
+int usage(const char* msg) {
+  std::fprintf(stderr, "worker: %s\n", msg);
+  return 2;
+}
+
+bool read_all(int fd, std::uint8_t* p, std::uint64_t n, std::uint64_t off) {
+  std::uint64_t got = 0;
+  while (got < n) {
+    const ssize_t r = ::pread(fd, p + got, n - got, static_cast<off_t>(off + got));
+    if (r < 0 && errno == EINTR) continue;
+    if (r <= 0) return false;
+    got += static_cast<std::uint64_t>(r);
+  }
+  return true;
+}
+
+}  // namespace
+
+int main(int argc, char** argv) {
+  if (argc < 2 || std::string(argv[1]) != "__worker") return usage("usage: paes_gpu_worker __worker --in ... --out ...");
+  std::string in, out, dir;
+  std::uint64_t offset = 0, len = 0;
+  int final_flag = -1, keyfd = -1, device = -1;
+  for (int i = 2; i + 1 < argc; i += 2) {
+    const std::string k = argv[i], v = argv[i + 1];
+    try {
+      if (k == "--in") in = v;
+      else if (k == "--out") out = v;
+      else if (k == "--dir") dir = v;
+      else if (k == "--offset") offset = std::stoull(v);
+      else if (k == "--len") len = std::stoull(v);
+      else if (k == "--final") final_flag = std::stoi(v);
+      else if (k == "--keyfd") keyfd = std::stoi(v);
+      else if (k == "--device") device = std::stoi(v);
+      else return usage(("unknown option " + k).c_str());
+    } catch (const std::exception&) {
+      return usage(("bad value for " + k).c_str());
+    }
+  }
+  if (in.empty() || out.empty() || final_flag < 0 || keyfd < 0) return usage("missing option");
+  int d = -1;
+  if (dir == "encrypt") d = PAES_ENCRYPT;
+  else if (dir == "decrypt") d = PAES_DECRYPT;
+  else return usage("bad --dir");
+
+  std::uint8_t key[16];
+  std::size_t got = 0;
+  while (got < 16) {
+    const ssize_t n = ::read(keyfd, key + got, 16 - got);
+    if (n <= 0) break;
+    got += static_cast<std::size_t>(n);
+  }
+  if (got != 16) {
+    std::fprintf(stderr, "worker: could not read 16 key bytes from fd %d\n", keyfd);
+    return 1;
+  }
+  if (keyfd != 0) ::close(keyfd);
+
+  const int ndev = paes_cuda_device_count();
+  if (ndev <= 0) {
+    std::fprintf(stderr, "worker: no CUDA device\n");
+    return 1;
+  }
+  if (device < 0 && std::getenv("PAES_WORKER_DEVICE")) device = std::atoi(std::getenv("PAES_WORKER_DEVICE"));
+  if (device < 0) device = static_cast<int>((len ? offset / len : 0) % static_cast<std::uint64_t>(ndev));
+  if (paes_cuda_set_devices(&device, 1) != PAES_OK) {
+    std::fprintf(stderr, "worker: %s\n", paes_cuda_last_error());
+    return 1;
+  }
+
+  const int fd = ::open(in.c_str(), O_RDONLY);
+  if (fd < 0) {
+    std::fprintf(stderr, "worker: cannot open input: %s\n", in.c_str());
+    return 1;
+  }
+  std::vector<std::uint8_t> raw(len), res(len + 16);
+  const bool ok = read_all(fd, raw.data(), len, offset);
+  ::close(fd);
+  if (!ok) {
+    std::fprintf(stderr, "worker: short read of chunk [%llu, +%llu): %s\n", static_cast<unsigned long long>(offset),
+                 static_cast<unsigned long long>(len), in.c_str());
+    return 1;
+  }
+  std::uint8_t rk[176];
+  paes_cuda_expand_key(key, rk);
+  std::uint64_t olen = 0;
+  const int rc = paes_cuda_chunk(d, raw.data(), len, final_flag, rk, res.data(), &olen, 1);
+  if (rc != PAES_OK) {
+    std::fprintf(stderr, "worker: %s\n", paes_cuda_last_error());
+    return rc == PAES_EINVAL ? 2 : 1;
+  }
+  FILE* f = std::fopen(out.c_str(), "wb");
+  if (!f) {
+    std::fprintf(stderr, "worker: cannot open output: %s\n", out.c_str());
+    return 1;
+  }
+  const bool wrote = olen == 0 || std::fwrite(res.data(), 1, olen, f) == olen;
+  if (std::fclose(f) != 0 || !wrote) {
+    std::fprintf(stderr, "worker: write failed: %s\n", out.c_str());
+    return 1;
+  }
+  return 0;
+}
