@@ -294,14 +294,42 @@ int paes_cuda_batch_host(int dir, const uint8_t* h_in, uint8_t* h_out, const uin
       write_batch_image(imgs[k], rin.data() + g.first, rout.data() + g.first, rks + 176ull * g.first,
                         host + img_off[k]);
     }
+    // persistent per-stream buffers: input span (the ring's dbuf), output
+    // span (obuf) and descriptor image (dsc) -- stream-ordered allocations
+    // per group would let the pool serialise groups across streams
+    if (d.obuf.empty()) {
+      for (int i = 0; i < S; ++i) {
+        std::uint8_t* p = nullptr;
+        PAES_CK(cudaMalloc(&p, C + 16));
+        d.obuf.push_back(p);
+        d.dsc.push_back(nullptr);
+        d.dsc_cap.push_back(0);
+      }
+    }
+    for (std::size_t k = 0; k < groups.size(); ++k) {
+      const BatchImage& b = imgs[k];
+      const int s = static_cast<int>(k % S);
+      if (d.dsc_cap[s] < b.total_bytes) {
+        PAES_CK(cudaStreamSynchronize(d.st[s]));
+        if (d.dsc[s]) PAES_CK(cudaFree(d.dsc[s]));
+        d.dsc[s] = nullptr;
+        d.dsc_cap[s] = 0;
+        PAES_CK(cudaMalloc(&d.dsc[s], b.total_bytes));
+        d.dsc_cap[s] = b.total_bytes;
+      }
+    }
     for (std::size_t k = 0; k < groups.size(); ++k) {
       const Group& g = groups[k];
       const BatchImage& b = imgs[k];
       cudaStream_t s = d.st[k % S];
-      std::uint8_t *din = nullptr, *dout = nullptr, *dd = nullptr;
-      PAES_CK(cudaMallocAsync(reinterpret_cast<void**>(&din), std::max<std::uint64_t>(16, g.in_hi - g.in_lo), s));
-      PAES_CK(cudaMallocAsync(reinterpret_cast<void**>(&dout), std::max<std::uint64_t>(16, g.out_hi - g.out_lo), s));
-      PAES_CK(cudaMallocAsync(reinterpret_cast<void**>(&dd), b.total_bytes, s));
+      const bool fits = g.in_hi - g.in_lo <= C + 16 && g.out_hi - g.out_lo <= C + 16;
+      std::uint8_t* din = d.dbuf[k % S];
+      std::uint8_t* dout = d.obuf[k % S];
+      std::uint8_t* dd = d.dsc[k % S];
+      if (!fits) {  // a single message larger than the staging chunk
+        PAES_CK(cudaMallocAsync(reinterpret_cast<void**>(&din), std::max<std::uint64_t>(16, g.in_hi - g.in_lo), s));
+        PAES_CK(cudaMallocAsync(reinterpret_cast<void**>(&dout), std::max<std::uint64_t>(16, g.out_hi - g.out_lo), s));
+      }
       if (g.in_hi > g.in_lo)
         PAES_CK(cudaMemcpyAsync(din, h_in + g.in_lo, g.in_hi - g.in_lo, cudaMemcpyHostToDevice, s));
       PAES_CK(cudaMemcpyAsync(dd, host + img_off[k], b.image_bytes, cudaMemcpyHostToDevice, s));
@@ -310,9 +338,10 @@ int paes_cuda_batch_host(int dir, const uint8_t* h_in, uint8_t* h_out, const uin
       if (b.check)
         PAES_CK(cudaMemcpyAsync(host + img_off[k] + b.status_off, dd + b.status_off, 4ull * b.n,
                                 cudaMemcpyDeviceToHost, s));
-      PAES_CK(cudaFreeAsync(din, s));
-      PAES_CK(cudaFreeAsync(dout, s));
-      PAES_CK(cudaFreeAsync(dd, s));
+      if (!fits) {
+        PAES_CK(cudaFreeAsync(din, s));
+        PAES_CK(cudaFreeAsync(dout, s));
+      }
     }
     for (auto s : d.st) PAES_CK(cudaStreamSynchronize(s));
     PAES_CK(cudaEventRecord(t_stage.ev, d.st[0]));

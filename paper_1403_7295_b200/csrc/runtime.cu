@@ -84,10 +84,15 @@ void ensure_pipeline(DevCtx& d, bool need_host) {
   if (d.chunk != chunk || static_cast<int>(d.st.size()) != ns) {
     for (auto p : d.dbuf) cudaFree(p);
     for (auto p : d.hbuf) cudaFreeHost(p);
+    for (auto p : d.obuf) cudaFree(p);
+    for (auto p : d.dsc) cudaFree(p);
     for (auto s : d.st) cudaStreamDestroy(s);
     for (auto e : d.ev) cudaEventDestroy(e);
     d.dbuf.clear();
     d.hbuf.clear();
+    d.obuf.clear();
+    d.dsc.clear();
+    d.dsc_cap.clear();
     d.st.clear();
     d.ev.clear();
     d.chunk = chunk;
@@ -156,8 +161,6 @@ std::uint64_t piece_size(std::uint64_t len, std::uint64_t chunk, int streams) {
   return std::clamp(p, floor_piece, chunk);
 }
 
-// Host range on one device through the stream ring (d.mu held).  Returns the
-// number of output bytes (decrypt+check: unpadded).
 // Small host ranges (<= kSmallBytes): one memcpy into a mapped pinned buffer,
 // ONE kernel that reads and writes that host buffer over PCIe (zero-copy),
 // one sync, one memcpy out.  Replaces H2D + launch + D2H (three commands and
@@ -273,6 +276,9 @@ std::uint64_t run_host_range_staged(DevCtx& d, const Range& r, const std::uint8_
   return out_total;
 }
 
+// Host range on one device (d.mu held): small -> zero-copy, pageable ->
+// staged ring, pinned -> direct ring.  Returns the number of output bytes
+// (decrypt with trailer check: unpadded).
 std::uint64_t run_host_range(DevCtx& d, const Range& r, const std::uint8_t* in, std::uint8_t* out, const KeyWords& kw) {
   DeviceGuard g(d.id);
   ensure_pipeline(d, false);

@@ -74,6 +74,9 @@ struct DevCtx {
   std::vector<cudaStream_t> st;
   std::vector<std::uint8_t*> dbuf;  // chunk + 16 bytes each
   std::vector<std::uint8_t*> hbuf;  // pinned staging for the file path
+  std::vector<std::uint8_t*> obuf;  // second device ring (batch output spans), chunk + 16 each, lazy
+  std::vector<std::uint8_t*> dsc;   // per-stream batch descriptor images, lazy, grow-only
+  std::vector<std::size_t> dsc_cap;
   std::vector<cudaEvent_t> ev;
   std::uint64_t chunk = 0;
   std::uint32_t* d_status = nullptr;
