@@ -260,6 +260,36 @@ def set_pipeline(chunk_bytes: int = 0, streams: int = 0) -> None:
     _raise(N.load().paes_cuda_set_pipeline(chunk_bytes, streams))
 
 
+def _tensor_call(direction: int, x, key: bytes, is_final: bool, out):
+    import torch
+
+    if not (isinstance(x, torch.Tensor) and x.is_cuda and x.dtype == torch.uint8):
+        raise ValueError("expected a CUDA uint8 tensor")
+    x = x.contiguous().view(-1)
+    n = x.numel()
+    cap = (n // 16 + 1) * 16 if (direction == ENCRYPT and is_final) else n
+    if out is None:
+        out = torch.empty(max(cap, 1), dtype=torch.uint8, device=x.device)
+    elif not (out.is_cuda and out.dtype == torch.uint8 and out.is_contiguous() and out.numel() >= cap):
+        raise ValueError(f"out must be a contiguous CUDA uint8 tensor of >= {cap} elements")
+    dev = x.device.index if x.device.index is not None else torch.cuda.current_device()
+    stream = torch.cuda.current_stream(dev).cuda_stream
+    m = chunk_device(direction, x.data_ptr(), n, is_final, round_keys(key), out.data_ptr(), dev, stream)
+    return out[:m]
+
+
+def encrypt_tensor(x, key: bytes, is_final: bool = True, out=None):
+    """encrypt_chunk on a CUDA uint8 tensor, on the current torch stream;
+    returns the ciphertext view (always-pad when is_final)."""
+    return _tensor_call(ENCRYPT, x, key, is_final, out)
+
+
+def decrypt_tensor(x, key: bytes, is_final: bool = True, out=None):
+    """decrypt_chunk on a CUDA uint8 tensor; a final chunk's trailer is checked
+    (PaddingError) and the returned view excludes the padding."""
+    return _tensor_call(DECRYPT, x, key, is_final, out)
+
+
 def ecb_device(direction: int, d_in: int, d_out: int, nbytes: int, rk: bytes, device: int = 0, stream: int = 0):
     """Device-resident ECB on raw pointers (asynchronous on `stream`)."""
     _raise(N.load().paes_cuda_ecb_device(direction, d_in, d_out, nbytes, rk, device, stream or None))
