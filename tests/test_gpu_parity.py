@@ -172,8 +172,9 @@ def test_chunk_device_tails_alignment_inplace(paes, gpu, orc):
 
 def test_chunk_device_wrong_key(paes, gpu):
     torch = _torch()
-    key = os.urandom(16)
-    ct = paes.encrypt_bytes(os.urandom(1000), key)
+    rnd = random.Random(175)  # deterministic: a random wrong key yields a valid trailer ~0.4% of the time
+    key = rnd.randbytes(16)
+    ct = paes.encrypt_bytes(rnd.randbytes(1000), key)
     src = dev_from_bytes(ct)
     dst = torch.zeros_like(src)
     bad = paes.round_keys(bytes([key[0] ^ 0x5A]) + key[1:])
@@ -443,7 +444,8 @@ def test_multi_shard_paths_on_one_device(paes, gpu, orc, tmp_path):
     times: same code path as 3 GPUs, shards serialise on the device lock."""
     paes.set_devices([0, 0, 0])
     try:
-        key = os.urandom(16)
+        rnd = random.Random(446)  # deterministic inputs: the wrong-key checks below must not flake
+        key = rnd.randbytes(16)
         for n in [0, 15, 16, 47, 48, 49, 1000, 100_003, 3 * 4096 + 5]:
             data = os.urandom(n)
             ct = paes.encrypt_chunk(data, True, key, ngpus=3)
@@ -452,11 +454,11 @@ def test_multi_shard_paths_on_one_device(paes, gpu, orc, tmp_path):
             if n % 16 == 0:
                 assert paes.encrypt_ecb(data, key, ngpus=3) == orc.ecb(0, data, key)
         # wrong key on a sharded buffer decrypt -> PaddingError (decrypt_chunk semantics)
-        ct = paes.encrypt_bytes(os.urandom(5000), key)
+        ct = paes.encrypt_bytes(rnd.randbytes(5000), key)
         with pytest.raises(paes.PaddingError):
             paes.decrypt_chunk(ct, True, bytes([key[0] ^ 1]) + key[1:], ngpus=3)
         # files: 3 shards, wrong key names the final chunk (exec.cpp:177-184)
-        data = os.urandom(200_001)
+        data = rnd.randbytes(200_001)
         (tmp_path / "p").write_bytes(data)
         o = paes.encrypt_file(str(tmp_path / "p"), str(tmp_path / "c"), key, workers=3)
         assert o["bytes_out"] == (len(data) // 16 + 1) * 16

@@ -37,8 +37,9 @@ def test_gpu_run_job_equals_reference_sequential(paes, gpu, ref, eight_workers, 
 
 
 def test_decrypt_inverts_encrypt_across_pairings(paes, gpu, ref, eight_workers, tmp_path):
-    key = os.urandom(16)
-    data = os.urandom(100_001)
+    rnd = random.Random(40)  # deterministic: the wrong-key check must not flake on a valid random trailer
+    key = rnd.randbytes(16)
+    data = rnd.randbytes(100_001)
     src = tmp_path / "plain.bin"
     src.write_bytes(data)
     for enc_w in (1, 3):
