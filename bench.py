@@ -499,6 +499,17 @@ def main():
     args = ap.parse_args()
     if args.warmup < 3 and os.environ.get("PAES_BENCH_ALLOW_SHORT") != "1":
         args.warmup = 3  # contract: >= 3 warm-up steps
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # --gpus N without a launcher: become N ranks (one process per GPU)
+        import socket
+
+        s = socket.socket()
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+        s.close()
+        os.execvp(sys.executable, [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+                                   f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+                                   f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:])
     # PAES_BENCH_SHARED_DEVICE=1: every rank on cuda:0 over gloo -- a plumbing
     # smoke of the N>1 path on a one-GPU box (ranks never wait on each other's
     # kernels; only CPU barriers and scalar reductions cross ranks).
