@@ -247,7 +247,7 @@ def run_reference(args, dist: Dist):
 
 
 def cpu_baseline(args):
-    R, key, pt, ct, workers, phys = reference_sample(args.total_bytes, args.seed, target_s=2.5)
+    R, key, pt, ct, workers, phys = reference_sample(args.total_bytes, args.seed, target_s=4.0)  # ~10-20 s of CPU work over 5 reps
     samples = []
     for _ in range(5):
         t = time.perf_counter()
