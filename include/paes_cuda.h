@@ -72,6 +72,11 @@ int paes_cuda_set_devices(const int* ids, int n);
 /* Host-pointer pipeline tuning: staging chunk (bytes, multiple of 16) and
  * streams per device (>= 1).  0 keeps the current value.  Defaults 64 MiB, 3. */
 int paes_cuda_set_pipeline(uint64_t chunk_bytes, int streams);
+/* Pinned host ranges up to this many bytes (per device shard) skip the copy
+ * ring: one kernel reads and writes the caller's pinned buffers over PCIe
+ * through their UVA aliases.  0 disables.  Default 128 MiB
+ * (profiles/r01_zero_copy_probe.json). */
+int paes_cuda_set_zero_copy_max(uint64_t bytes);
 
 /* ---- host-side rules (no GPU needed) ------------------------------------ */
 

@@ -44,6 +44,13 @@ int paes_cuda_set_pipeline(uint64_t chunk_bytes, int streams) {
   });
 }
 
+int paes_cuda_set_zero_copy_max(uint64_t bytes) {
+  return guarded([&] {
+    set_zero_copy_max(bytes);
+    return PAES_OK;
+  });
+}
+
 int paes_cuda_expand_key(const uint8_t key[16], uint8_t rk[176]) {
   return guarded([&] {
     if (!key || !rk) throw std::invalid_argument("null key");
@@ -157,12 +164,12 @@ int paes_cuda_chunk_device(int dir, const void* d_in, uint64_t len, int is_final
     }
     std::lock_guard<std::mutex> lk(d.mu);
     EcbArgs a = make_args(r, static_cast<const std::uint8_t*>(d_in), static_cast<std::uint8_t*>(d_out), len, true,
-                          dec_key_words(rk), d.d_status);
-    PAES_CK(cudaMemsetAsync(d.d_status, 0xff, 4, s));
+                          dec_key_words(rk), d.m_status);
+    // the trailer check writes the mapped word itself: no memset / D2H copy
+    *reinterpret_cast<volatile std::uint32_t*>(d.h_status) = 0xffffffffu;  // sentinel: unchecked => PaddingError
     PAES_CK(launch_ecb(true, a, d.sm_count, s));
-    PAES_CK(cudaMemcpyAsync(d.h_status, d.d_status, 4, cudaMemcpyDeviceToHost, s));
     PAES_CK(cudaStreamSynchronize(s));
-    const std::uint32_t k = *d.h_status;
+    const std::uint32_t k = *reinterpret_cast<volatile std::uint32_t*>(d.h_status);
     if (k == 0xffffffffu) throw PaddingError("unpad: invalid pad bytes");
     if (out_len) *out_len = len - k;
     return PAES_OK;

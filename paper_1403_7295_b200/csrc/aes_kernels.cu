@@ -201,9 +201,6 @@ __device__ __forceinline__ std::uint32_t pad_check(const Block4& b) {
 template <bool DEC, int NB, bool ALIGNED>
 __global__ void __launch_bounds__(kThreads, 1) ecb_kernel(const __grid_constant__ EcbArgs a) {
   extern __shared__ __align__(16) std::uint32_t sm[];
-  stage_tables<DEC>(sm);
-  __syncthreads();
-  const char* smb = reinterpret_cast<const char*>(sm);
   const std::uint32_t lane = threadIdx.x & 31;
   const std::uint32_t lane4 = lane * 4;
   constexpr unsigned long long kTile = 32ull * NB;
@@ -219,12 +216,17 @@ __global__ void __launch_bounds__(kThreads, 1) ecb_kernel(const __grid_constant_
   // The next tile's blocks are loaded before the current tile is computed
   // (register double buffer), so a warp never waits on HBM at a tile start --
   // otherwise the SM's warps, which advance in near lockstep on short
-  // launches, all stall on the same load latency together.
+  // launches, all stall on the same load latency together.  The first tile's
+  // loads are issued before the tables are staged, so their HBM latency hides
+  // behind the staging (this is most of a small launch's duration).
   Block4 nxt[NB];
   if (tile < full_tiles) {
 #pragma unroll
     for (int j = 0; j < NB; ++j) nxt[j] = load_block<ALIGNED>(a.in + 16ull * (tile * kTile + lane + 32ull * j));
   }
+  stage_tables<DEC>(sm);
+  __syncthreads();
+  const char* smb = reinterpret_cast<const char*>(sm);
   for (; tile < full_tiles; tile += tstride) {
     const unsigned long long b0 = tile * kTile + lane;
     Block4 s[NB];

@@ -7,6 +7,7 @@
 // run_job's strategy dispatch (exec.cpp:340-347).  Exceptions become codes:
 // std::invalid_argument -> PAES_EINVAL, PaddingError -> PAES_EBADMSG,
 // IoError -> PAES_EIO, WorkerError -> PAES_EWORKER, CUDA -> PAES_ECUDA.
+#include <atomic>
 #include <cuda_runtime.h>
 #include <fcntl.h>
 #include <sys/mman.h>
@@ -41,6 +42,7 @@ std::mutex g_cfg_mu;
 std::vector<int> g_devices;  // empty = all visible
 std::uint64_t g_chunk = 64ull << 20;  // scripts/pcie_probe.py: 64-128 MiB pieces reach ~94% of concurrent H2D+D2H
 int g_streams = 3;
+std::atomic<std::uint64_t> g_zero_copy_max{128ull << 20};  // scripts/zero_copy_probe.cu
 
 int visible_devices() {
   int n = 0;
@@ -62,8 +64,8 @@ DevCtx& device(int id) {
     DeviceGuard g(id);
     PAES_CK(cudaDeviceGetAttribute(&d.sm_count, cudaDevAttrMultiProcessorCount, id));
     PAES_CK(prepare_kernels());
-    PAES_CK(cudaMalloc(&d.d_status, 4096));
-    PAES_CK(cudaMallocHost(&d.h_status, 4096));
+    PAES_CK(cudaHostAlloc(reinterpret_cast<void**>(&d.h_status), 4096, cudaHostAllocMapped | cudaHostAllocPortable));
+    PAES_CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&d.m_status), d.h_status, 0));
     PAES_CK(cudaMalloc(&d.d_acc, 64));
     PAES_CK(cudaMallocHost(&d.h_acc, 64));
     d.id = id;
@@ -200,13 +202,39 @@ std::uint64_t run_small(DevCtx& d, const Range& r, const std::uint8_t* in, std::
   return olen;
 }
 
-bool is_pinned(const void* p) {
+// Device alias of a page-locked host pointer (under UVA every cudaHostAlloc'd
+// or registered buffer is device-accessible), or nullptr for pageable memory.
+const void* pinned_alias(const void* p) {
+  if (!p) return nullptr;
   cudaPointerAttributes a{};
   if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
     cudaGetLastError();
-    return false;
+    return nullptr;
   }
-  return a.type == cudaMemoryTypeHost;
+  return a.type == cudaMemoryTypeHost ? a.devicePointer : nullptr;
+}
+
+bool is_pinned(const void* p) { return pinned_alias(p) != nullptr; }
+
+// Pinned host ranges up to g_zero_copy_max: ONE kernel reads and writes the
+// caller's buffers over PCIe through their UVA aliases -- no device ring, no
+// copy-engine commands, no per-piece latencies.  Measured against the copy
+// ring (profiles/r01_zero_copy_probe.json): 3.4x at 1 MiB, ahead up to
+// ~256 MiB; beyond that the copy engines' larger PCIe requests win (46 vs
+// 40 GB/s at 1 GiB).
+std::uint64_t run_zero_copy(DevCtx& d, const Range& r, const void* din, void* dout, const KeyWords& kw) {
+  if (r.check_pad) *reinterpret_cast<volatile std::uint32_t*>(d.h_status) = 0xffffffffu;  // unchecked => PaddingError
+  EcbArgs a = make_args(r, static_cast<const std::uint8_t*>(din), static_cast<std::uint8_t*>(dout), r.in_len, true, kw,
+                        d.m_status);
+  PAES_CK(launch_ecb(r.dec, a, d.sm_count, d.st[0]));
+  PAES_CK(cudaStreamSynchronize(d.st[0]));
+  std::uint64_t olen = a.nblocks * 16;
+  if (r.check_pad) {
+    const std::uint32_t k = *reinterpret_cast<volatile std::uint32_t*>(d.h_status);
+    if (k == 0xffffffffu) throw PaddingError("unpad: invalid pad bytes");
+    olen -= k;
+  }
+  return olen;
 }
 
 // memcpy split over host threads (a single core moves ~10 GB/s; the pinned
@@ -247,6 +275,8 @@ std::uint64_t run_host_range_staged(DevCtx& d, const Range& r, const std::uint8_
     par_copy(out + pend_off[s], d.hbuf[s], pend_len[s]);
     pend_off[s] = -1;
   };
+  // the last piece's trailer check writes the mapped status word directly
+  if (r.check_pad) *reinterpret_cast<volatile std::uint32_t*>(d.h_status) = 0xffffffffu;  // unchecked => PaddingError
   std::uint64_t out_total = 0;
   for (std::uint64_t k = 0; k < npieces; ++k) {
     const int s = static_cast<int>(k % S);
@@ -255,13 +285,11 @@ std::uint64_t run_host_range_staged(DevCtx& d, const Range& r, const std::uint8_
     const std::uint64_t len = std::min<std::uint64_t>(C, r.in_len - off);
     const bool last = k + 1 == npieces;
     par_copy(d.hbuf[s], in + off, len);
-    EcbArgs a = make_args(r, d.dbuf[s], d.dbuf[s], len, last, kw, d.d_status);
+    EcbArgs a = make_args(r, d.dbuf[s], d.dbuf[s], len, last, kw, d.m_status);
     if (len) PAES_CK(cudaMemcpyAsync(d.dbuf[s], d.hbuf[s], len, cudaMemcpyHostToDevice, d.st[s]));
-    if (a.check_pad) PAES_CK(cudaMemsetAsync(d.d_status, 0xff, 4, d.st[s]));
     PAES_CK(launch_ecb(r.dec, a, d.sm_count, d.st[s]));
     const std::uint64_t olen = a.nblocks * 16;
     if (olen) PAES_CK(cudaMemcpyAsync(d.hbuf[s], d.dbuf[s], olen, cudaMemcpyDeviceToHost, d.st[s]));
-    if (last && a.check_pad) PAES_CK(cudaMemcpyAsync(d.h_status, d.d_status, 4, cudaMemcpyDeviceToHost, d.st[s]));
     PAES_CK(cudaEventRecord(d.ev[s], d.st[s]));
     pend_off[s] = static_cast<std::int64_t>(off);
     pend_len[s] = olen;
@@ -269,43 +297,49 @@ std::uint64_t run_host_range_staged(DevCtx& d, const Range& r, const std::uint8_
   }
   for (int s = 0; s < S; ++s) drain(s);
   if (r.check_pad) {
-    const std::uint32_t k = *d.h_status;
+    const std::uint32_t k = *reinterpret_cast<volatile std::uint32_t*>(d.h_status);
     if (k == 0xffffffffu) throw PaddingError("unpad: invalid pad bytes");
     out_total -= k;
   }
   return out_total;
 }
 
-// Host range on one device (d.mu held): small -> zero-copy, pageable ->
-// staged ring, pinned -> direct ring.  Returns the number of output bytes
+// Host range on one device (d.mu held): pinned up to g_zero_copy_max ->
+// zero-copy kernel on the caller's buffers; small pageable -> zero-copy via
+// the mapped bounce buffer; pageable -> staged ring; large pinned -> direct
+// ring.  Returns the number of output bytes
 // (decrypt with trailer check: unpadded).
 std::uint64_t run_host_range(DevCtx& d, const Range& r, const std::uint8_t* in, std::uint8_t* out, const KeyWords& kw) {
   DeviceGuard g(d.id);
   ensure_pipeline(d, false);
+  if (r.in_len && r.in_len <= g_zero_copy_max.load(std::memory_order_relaxed)) {
+    const void* din = pinned_alias(in);
+    const void* dout = din ? pinned_alias(out) : nullptr;
+    if (din && dout) return run_zero_copy(d, r, din, const_cast<void*>(dout), kw);
+  }
   if (r.in_len <= std::min(kSmallBytes, d.chunk)) return run_small(d, r, in, out, kw);
   if (!is_pinned(in) || !is_pinned(out)) return run_host_range_staged(d, r, in, out, kw);
   const int S = static_cast<int>(d.st.size());
   const std::uint64_t C = piece_size(r.in_len, d.chunk, S);
   const std::uint64_t npieces = std::max<std::uint64_t>(1, (r.in_len + C - 1) / C);
+  // the last piece's trailer check writes the mapped status word directly
+  if (r.check_pad) *reinterpret_cast<volatile std::uint32_t*>(d.h_status) = 0xffffffffu;  // unchecked => PaddingError
   std::uint64_t out_total = 0;
   for (std::uint64_t k = 0; k < npieces; ++k) {
     const int s = static_cast<int>(k % S);
     const std::uint64_t off = k * C;
     const std::uint64_t len = std::min<std::uint64_t>(C, r.in_len - off);
     const bool last = k + 1 == npieces;
-    EcbArgs a = make_args(r, d.dbuf[s], d.dbuf[s], len, last, kw, d.d_status);
+    EcbArgs a = make_args(r, d.dbuf[s], d.dbuf[s], len, last, kw, d.m_status);
     if (len) PAES_CK(cudaMemcpyAsync(d.dbuf[s], in + off, len, cudaMemcpyHostToDevice, d.st[s]));
-    if (a.check_pad) PAES_CK(cudaMemsetAsync(d.d_status, 0xff, 4, d.st[s]));  // sentinel: unchecked => PaddingError
     PAES_CK(launch_ecb(r.dec, a, d.sm_count, d.st[s]));
     const std::uint64_t olen = a.nblocks * 16;
     if (olen) PAES_CK(cudaMemcpyAsync(out + off, d.dbuf[s], olen, cudaMemcpyDeviceToHost, d.st[s]));
-    if (last && a.check_pad)
-      PAES_CK(cudaMemcpyAsync(d.h_status, d.d_status, 4, cudaMemcpyDeviceToHost, d.st[s]));
     out_total = off + olen;
   }
   for (auto s : d.st) PAES_CK(cudaStreamSynchronize(s));
   if (r.check_pad) {
-    const std::uint32_t k = *d.h_status;
+    const std::uint32_t k = *reinterpret_cast<volatile std::uint32_t*>(d.h_status);
     if (k == 0xffffffffu) throw PaddingError("unpad: invalid pad bytes");
     out_total -= k;
   }
@@ -370,6 +404,8 @@ void set_device_list(const std::vector<int>& ids) {
   std::lock_guard<std::mutex> lk(g_cfg_mu);
   g_devices = ids;
 }
+
+void set_zero_copy_max(std::uint64_t bytes) { g_zero_copy_max.store(bytes, std::memory_order_relaxed); }
 
 void set_pipeline_config(std::uint64_t chunk_bytes, int streams) {
   std::lock_guard<std::mutex> lk(g_cfg_mu);

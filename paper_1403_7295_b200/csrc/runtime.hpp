@@ -79,8 +79,8 @@ struct DevCtx {
   std::vector<std::size_t> dsc_cap;
   std::vector<cudaEvent_t> ev;
   std::uint64_t chunk = 0;
-  std::uint32_t* d_status = nullptr;
-  std::uint32_t* h_status = nullptr;  // pinned
+  std::uint32_t* h_status = nullptr;  // pinned, mapped
+  std::uint32_t* m_status = nullptr;  // device alias of h_status: a one-shot check writes it directly
   unsigned long long* d_acc = nullptr;
   unsigned long long* h_acc = nullptr;  // pinned
 };
@@ -96,6 +96,7 @@ void ensure_pipeline(DevCtx& d, bool need_host);
 std::vector<int> device_list(int ngpus);
 void set_device_list(const std::vector<int>& ids);
 void set_pipeline_config(std::uint64_t chunk_bytes, int streams);
+void set_zero_copy_max(std::uint64_t bytes);
 
 // ------------------------------------------------------------ pieces
 // A transform over one contiguous range: whole input blocks, plus (encrypt,

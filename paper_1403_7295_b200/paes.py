@@ -260,6 +260,12 @@ def set_pipeline(chunk_bytes: int = 0, streams: int = 0) -> None:
     _raise(N.load().paes_cuda_set_pipeline(chunk_bytes, streams))
 
 
+def set_zero_copy_max(nbytes: int) -> None:
+    """Pinned host ranges up to ``nbytes`` run as one zero-copy kernel on the
+    caller's buffers (0 = always use the copy-engine ring)."""
+    _raise(N.load().paes_cuda_set_zero_copy_max(nbytes))
+
+
 def _tensor_call(direction: int, x, key: bytes, is_final: bool, out):
     import torch
 

@@ -1,8 +1,10 @@
-"""The three host-pointer paths of paes_cuda_chunk, each forced explicitly:
-zero-copy small ranges, the pinned direct ring, and the staged ring for
-pageable memory -- all bit-exact vs the oracle across piece boundaries."""
+"""The host-pointer paths of paes_cuda_chunk, each forced explicitly: the
+zero-copy kernel on pinned buffers, the pinned direct ring (zero-copy off),
+the mapped bounce buffer for small pageable ranges and the staged ring for
+pageable memory -- all bit-exact vs the oracle across piece boundaries, and
+each rejecting a wrong key."""
 import ctypes as C
-import os
+import random
 
 import numpy as np
 import pytest
@@ -11,24 +13,28 @@ pytestmark = pytest.mark.gpu
 MiB = 1 << 20
 
 
-def _run(paes, direction, src_ptr, n, final, key, dst_ptr):
+def _run(paes, direction, src_ptr, n, final, key, dst_ptr, expect_rc=0):
     from paper_1403_7295_b200 import _native as N
 
     olen = C.c_uint64()
     rc = N.load().paes_cuda_chunk(direction, src_ptr, n, int(final), paes.round_keys(key), dst_ptr, C.byref(olen), 1)
-    assert rc == 0, N.last_error()
+    assert rc == expect_rc, N.last_error()
     return olen.value
 
 
-@pytest.mark.parametrize("pinned", [True, False])
-def test_ring_paths_vs_oracle(paes, gpu, orc, pinned):
+@pytest.mark.parametrize("mode", ["pinned_zero_copy", "pinned_ring", "pageable"])
+def test_ring_paths_vs_oracle(paes, gpu, orc, mode):
     import torch
 
+    pinned = mode != "pageable"
     paes.set_pipeline(64 * 1024, 3)  # tiny pieces: many slots in flight, small-path threshold 64 KiB
+    paes.set_zero_copy_max(0 if mode == "pinned_ring" else 128 * MiB)
+    rnd = random.Random(hash(mode) & 0xFFFF)
     try:
-        key = os.urandom(16)
+        key = rnd.randbytes(16)
+        bad = bytes([key[0] ^ 0x80]) + key[1:]
         for n in [100, 64 * 1024, 64 * 1024 + 1, 3 * 64 * 1024 + 7, 1_000_003]:
-            data = os.urandom(n)
+            data = rnd.randbytes(n)
             if pinned:
                 src = torch.empty(n + 32, dtype=torch.uint8, pin_memory=True)
                 dst = torch.empty(n + 32, dtype=torch.uint8, pin_memory=True)
@@ -46,5 +52,17 @@ def test_ring_paths_vs_oracle(paes, gpu, orc, pinned):
             # decrypt back (in place in the output buffer)
             k = _run(paes, 1, dp, m, True, key, dp)
             assert k == n and read(n) == data, (n, pinned)
+            # a wrong key fails the trailer check on this path too (EBADMSG)
+            m = _run(paes, 0, sp, n, True, key, dp)
+            try:
+                expect = orc.decrypt_chunk(want, True, bad)
+            except ValueError:
+                expect = None
+            if expect is None:
+                _run(paes, 1, dp, m, True, bad, dp, expect_rc=-74)
+            else:  # the wrong key happened to leave a valid trailer: same bytes as the oracle
+                k = _run(paes, 1, dp, m, True, bad, dp)
+                assert read(k) == expect
     finally:
         paes.set_pipeline(64 * MiB, 3)
+        paes.set_zero_copy_max(128 * MiB)
