@@ -69,8 +69,9 @@ int paes_cuda_device_count(void);
  * all visible devices).  ngpus = k uses the first k of this list.  n = 0
  * restores the default.  One process per GPU (torchrun) sets {local_rank}. */
 int paes_cuda_set_devices(const int* ids, int n);
-/* Host-pointer pipeline tuning: staging chunk (bytes, multiple of 16) and
- * streams per device (>= 1).  0 keeps the current value.  Defaults 64 MiB, 3. */
+/* Host-pointer pipeline tuning: staging chunk (bytes, a multiple of 16 and
+ * >= 4096) and streams per device (1..32).  0 keeps the current value.
+ * Defaults 64 MiB, 3. */
 int paes_cuda_set_pipeline(uint64_t chunk_bytes, int streams);
 /* Pinned host ranges up to this many bytes (per device shard) skip the copy
  * ring: one kernel reads and writes the caller's pinned buffers over PCIe

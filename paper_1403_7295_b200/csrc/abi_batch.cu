@@ -248,6 +248,7 @@ int paes_cuda_batch_host(int dir, const uint8_t* h_in, uint8_t* h_out, const uin
     DeviceGuard dg(device_id);
     std::lock_guard<std::mutex> lk(d.mu);
     ensure_pipeline(d, false);
+    QuiesceOnThrow quiesce{d};
     const std::uint64_t C = d.chunk;
     const int S = static_cast<int>(d.st.size());
     // groups of consecutive messages whose input and output spans stay <= C

@@ -38,7 +38,8 @@ int paes_cuda_set_devices(const int* ids, int n) {
 int paes_cuda_set_pipeline(uint64_t chunk_bytes, int streams) {
   return guarded([&] {
     if (chunk_bytes % 16 != 0) throw std::invalid_argument("chunk_bytes must be a multiple of 16");
-    if (streams < 0) throw std::invalid_argument("streams must be >= 0");
+    if (chunk_bytes && chunk_bytes < 4096) throw std::invalid_argument("chunk_bytes must be >= 4096");
+    if (streams < 0 || streams > 32) throw std::invalid_argument("streams must be in [0, 32]");
     set_pipeline_config(chunk_bytes, streams);
     return PAES_OK;
   });

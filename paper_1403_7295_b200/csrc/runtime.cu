@@ -264,6 +264,7 @@ void par_copy(std::uint8_t* dst, const std::uint8_t* src, std::uint64_t n) {
 std::uint64_t run_host_range_staged(DevCtx& d, const Range& r, const std::uint8_t* in, std::uint8_t* out,
                                     const KeyWords& kw) {
   ensure_pipeline(d, true);
+  QuiesceOnThrow quiesce{d};
   const int S = static_cast<int>(d.st.size());
   const std::uint64_t C = piece_size(r.in_len, d.chunk, S);
   const std::uint64_t npieces = std::max<std::uint64_t>(1, (r.in_len + C - 1) / C);
@@ -319,6 +320,7 @@ std::uint64_t run_host_range(DevCtx& d, const Range& r, const std::uint8_t* in, 
   }
   if (r.in_len <= std::min(kSmallBytes, d.chunk)) return run_small(d, r, in, out, kw);
   if (!is_pinned(in) || !is_pinned(out)) return run_host_range_staged(d, r, in, out, kw);
+  QuiesceOnThrow quiesce{d};
   const int S = static_cast<int>(d.st.size());
   const std::uint64_t C = piece_size(r.in_len, d.chunk, S);
   const std::uint64_t npieces = std::max<std::uint64_t>(1, (r.in_len + C - 1) / C);

@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <exception>
 #include <mutex>
 #include <stdexcept>
 #include <string>
@@ -92,6 +93,18 @@ int visible_devices();
 DevCtx& device(int id);
 // Pipeline buffers (device ring, optional pinned host ring); d.mu held.
 void ensure_pipeline(DevCtx& d, bool need_host);
+// Drains a device's ring streams when its scope is left by an exception: the
+// copies and kernels already queued still target the caller's buffers and the
+// ring's slots, so returning an error code before they finish would hand the
+// caller buffers under live DMA.
+struct QuiesceOnThrow {
+  DevCtx& d;
+  int depth = std::uncaught_exceptions();
+  ~QuiesceOnThrow() {
+    if (std::uncaught_exceptions() > depth)
+      for (auto s : d.st) cudaStreamSynchronize(s);
+  }
+};
 // The devices host-pointer calls shard over (first `ngpus`, 0 = all).
 std::vector<int> device_list(int ngpus);
 void set_device_list(const std::vector<int>& ids);

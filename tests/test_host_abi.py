@@ -194,6 +194,10 @@ def test_argument_errors_before_device(paes):
     assert L.paes_cuda_ecb(7, None, None, 0, paes.round_keys(bytes(16)), 0) == N.EINVAL
     assert L.paes_cuda_set_pipeline(15, 0) == N.EINVAL
     assert b"multiple of 16" in L.paes_cuda_last_error()
+    assert L.paes_cuda_set_pipeline(16, 0) == N.EINVAL  # below the 4 KiB floor
+    assert L.paes_cuda_set_pipeline(0, 33) == N.EINVAL
+    assert L.paes_cuda_set_pipeline(0, -1) == N.EINVAL
+    assert L.paes_cuda_set_pipeline(0, 0) == 0  # 0 keeps the current values
 
 
 def test_missing_library_raises(tmp_path, monkeypatch):
