@@ -50,6 +50,8 @@ BatchImage plan_batch(int dir, const uint64_t* in_off, const uint64_t* out_off, 
     if (b.check && lens[i] == 0) throw PaddingError("unpad: length must be a non-zero multiple of 16");
     const unsigned long long nb = lens[i] / 16 + ((pad && !b.dec) ? 1 : 0);
     if (nb > 0xffffffffull) throw std::invalid_argument("message too large for the batch path");
+    if (lens[i] > UINT64_MAX - in_off[i] || 16 * nb > UINT64_MAX - out_off[i])
+      throw std::invalid_argument("batch message span overflows the address range");
     b.nblocks[i] = static_cast<std::uint32_t>(nb);
     b.total_tiles += (nb + batch_tile_blocks() - 1) / batch_tile_blocks();
   }
@@ -118,7 +120,8 @@ thread_local Staging t_stage;
 
 std::uint8_t* staging(std::size_t bytes, int device) {
   Staging& st = t_stage;
-  if (st.ev && st.device == device) PAES_CK(cudaEventSynchronize(st.ev));
+  // the previous upload (on whichever device) must finish reading the buffer
+  if (st.ev) PAES_CK(cudaEventSynchronize(st.ev));
   if (st.device != device) {
     if (st.ev) cudaEventDestroy(st.ev);
     st.ev = nullptr;

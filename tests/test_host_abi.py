@@ -207,3 +207,17 @@ def test_missing_library_raises(tmp_path, monkeypatch):
     monkeypatch.setattr(_native, "lib_path", lambda: str(tmp_path / "nope.so"))
     with pytest.raises(_native.NativeLibraryMissing):
         _native.load()
+
+
+def test_batch_descriptor_errors_before_device(paes):
+    """plan_batch validates every descriptor before touching a device."""
+    rk = paes.round_keys(bytes(16))
+    with pytest.raises(ValueError, match="multiples of 16"):
+        paes.ecb_batch(0, 1, 1, [8], [0], [16], rk, True)
+    with pytest.raises(ValueError, match="overflows"):
+        paes.ecb_batch(0, 1, 1, [(1 << 64) - 16], [0], [32], rk, True)
+    with pytest.raises(ValueError, match="overflows"):
+        paes.ecb_batch_host(0, 1, 1, [0], [(1 << 64) - 16], [16], rk, True)
+    with pytest.raises(paes.PaddingError):
+        paes.ecb_batch(1, 1, 1, [0], [0], [0], rk, True)
+    assert paes.ecb_batch(0, 0, 0, [], [], [], b"", True) == []
