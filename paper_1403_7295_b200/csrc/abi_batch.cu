@@ -6,6 +6,7 @@
 #include <algorithm>
 #include <cstring>
 #include <memory>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -145,6 +146,7 @@ struct paes_batch_plan {
   BatchImage img;
   std::uint8_t* dd = nullptr;        // device image
   std::uint32_t* h_status = nullptr;  // pinned
+  std::mutex check_mu;  // checked runs share the status words: one at a time
 };
 
 extern "C" {
@@ -211,14 +213,16 @@ int paes_cuda_batch_plan_run(paes_batch_plan* plan, const void* d_in, void* d_ou
     DevCtx& d = device(plan->device);
     DeviceGuard dg(plan->device);
     cudaStream_t s = static_cast<cudaStream_t>(stream);
-    PAES_CK(launch_batch(b.dec, batch_args(b, d_in, d_out, plan->dd), d.sm_count, s));
-    if (b.check) {
-      PAES_CK(cudaMemcpyAsync(plan->h_status, plan->dd + b.status_off, 4ull * b.n, cudaMemcpyDeviceToHost, s));
-      PAES_CK(cudaStreamSynchronize(s));
-      finish_lengths(b, plan->h_status, out_lens);
-    } else {
+    if (!b.check) {  // descriptors are read-only: unchecked runs may overlap freely
+      PAES_CK(launch_batch(b.dec, batch_args(b, d_in, d_out, plan->dd), d.sm_count, s));
       finish_lengths(b, nullptr, out_lens);
+      return PAES_OK;
     }
+    std::lock_guard<std::mutex> lk(plan->check_mu);
+    PAES_CK(launch_batch(b.dec, batch_args(b, d_in, d_out, plan->dd), d.sm_count, s));
+    PAES_CK(cudaMemcpyAsync(plan->h_status, plan->dd + b.status_off, 4ull * b.n, cudaMemcpyDeviceToHost, s));
+    PAES_CK(cudaStreamSynchronize(s));
+    finish_lengths(b, plan->h_status, out_lens);
     return PAES_OK;
   });
 }

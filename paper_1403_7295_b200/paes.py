@@ -352,7 +352,6 @@ class BatchPlan:
         import numpy as np
 
         self.n = len(lens)
-        self._olens = np.zeros(max(self.n, 1), dtype=np.uint64)
         h = C.c_void_p()
         a, b, c = _u64_array(in_off), _u64_array(out_off), _u64_array(lens)
         _raise(N.load().paes_cuda_batch_plan_create(direction, a[1], b[1], c[1], rks, self.n, int(bool(pad)), device,
@@ -360,9 +359,13 @@ class BatchPlan:
         self._h = h
 
     def run(self, d_in: int, d_out: int, stream: int = 0):
-        _raise(N.load().paes_cuda_batch_plan_run(self._h, d_in, d_out,
-                                                 self._olens.ctypes.data_as(C.POINTER(C.c_uint64)), stream or None))
-        return self._olens[: self.n].tolist()
+        """One launch; thread-safe (each call has its own output lengths)."""
+        import numpy as np
+
+        olens = np.zeros(max(self.n, 1), dtype=np.uint64)
+        _raise(N.load().paes_cuda_batch_plan_run(self._h, d_in, d_out, olens.ctypes.data_as(C.POINTER(C.c_uint64)),
+                                                 stream or None))
+        return olens[: self.n].tolist()
 
     def close(self):
         if getattr(self, "_h", None) is not None and self._h.value:

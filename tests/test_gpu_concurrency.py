@@ -63,3 +63,39 @@ def test_concurrent_mixed_calls(paes, gpu, orc):
     with ThreadPoolExecutor(12) as ex:
         done = list(ex.map(run, jobs))
     assert len(done) == len(jobs)
+
+
+def test_one_checked_plan_from_many_threads(paes, gpu, orc):
+    """A decrypt plan with trailer checks run concurrently on several streams:
+    the shared status words are serialised, every run sees its own lengths."""
+    import torch
+
+    rnd = random.Random(5)
+    lens = [rnd.randrange(0, 40_000) for _ in range(37)]
+    keys = [rnd.randbytes(16) for _ in lens]
+    msgs = [rnd.randbytes(n) for n in lens]
+    cts = [orc.encrypt_chunk(m, True, k) for m, k in zip(msgs, keys)]
+    offs, o = [], 0
+    for c in cts:
+        offs.append(o)
+        o += len(c)
+    src = torch.from_numpy(np.frombuffer(b"".join(cts), dtype=np.uint8).copy()).cuda()
+    rks = b"".join(paes.round_keys(k) for k in keys)
+    plan = paes.BatchPlan(paes.DECRYPT, offs, offs, [len(c) for c in cts], rks, True)
+
+    def worker(t):
+        stream = torch.cuda.Stream()
+        dst = torch.zeros(o, dtype=torch.uint8, device="cuda")
+        for _ in range(10):
+            with torch.cuda.stream(stream):
+                got = plan.run(src.data_ptr(), dst.data_ptr(), stream.cuda_stream)
+            assert got == lens, t
+        stream.synchronize()
+        h = dst.cpu().numpy()
+        return all(h[off:off + n].tobytes() == m for off, n, m in zip(offs, lens, msgs))
+
+    try:
+        with ThreadPoolExecutor(4) as ex:
+            assert all(ex.map(worker, range(4)))
+    finally:
+        plan.close()
