@@ -48,6 +48,15 @@ extern "C" {
 #define PAES_ENCRYPT 0
 #define PAES_DECRYPT 1
 
+/* Single-state round transforms (aes.hpp:72-78). */
+#define PAES_OP_SUB_BYTES 0
+#define PAES_OP_INV_SUB_BYTES 1
+#define PAES_OP_SHIFT_ROWS 2
+#define PAES_OP_INV_SHIFT_ROWS 3
+#define PAES_OP_MIX_COLUMNS 4
+#define PAES_OP_INV_MIX_COLUMNS 5
+#define PAES_OP_ADD_ROUND_KEY 6
+
 /* ChunkSpec (chunk.hpp:20-27), padded to a fixed 32-byte C layout. */
 typedef struct paes_chunk_spec {
   uint64_t offset;
@@ -94,6 +103,17 @@ int64_t paes_cuda_plan_decrypt_chunks(uint64_t cipher_len, uint32_t workers, pae
 int64_t paes_cuda_pad_final(const uint8_t* raw, uint64_t len, uint8_t* out);
 /* unpad_final (chunk.hpp:52-54, chunk.cpp:90-100): unpadded length or PAES_EBADMSG. */
 int64_t paes_cuda_unpad_final(const uint8_t* padded, uint64_t len);
+
+/* ---- single-state API (the reference's KAT / test face) -----------------
+ * sub_bytes, inv_sub_bytes, shift_rows, inv_shift_rows, mix_columns,
+ * inv_mix_columns, add_round_key (aes.hpp:72-78, aes.cpp:194-227) applied in
+ * place to n independent 16-byte states (host memory; byte i = row i%4,
+ * column i/4) on the first listed device.  rk16 is the round key for
+ * PAES_OP_ADD_ROUND_KEY and ignored otherwise.  Synchronous. */
+int paes_cuda_state_transform(int op, uint8_t* states, uint64_t n, const uint8_t rk16[16]);
+/* sbox() / inv_sbox() (aes.hpp:69-70, aes.cpp:184-192): the library's
+ * compile-time tables (aes_tables.hpp), 256 bytes. */
+int paes_cuda_sbox(int inverse, uint8_t out[256]);
 
 /* ---- bulk ECB: the hot path ---------------------------------------------
  * aes::encrypt_ecb / decrypt_ecb (aes.hpp:84-89, aes.cpp:241-265).

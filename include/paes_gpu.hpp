@@ -9,6 +9,8 @@
 //   aes::Key128, aes::RoundKeySchedule          gpu::Key128, gpu::RoundKeySchedule   (aes.hpp:19-50)
 //   aes::encrypt_ecb / decrypt_ecb              gpu::encrypt_ecb / decrypt_ecb       (aes.hpp:86-89)
 //   aes::encrypt_block / decrypt_block          gpu::encrypt_block / decrypt_block   (aes.hpp:81-82)
+//   aes::State, gf_xtime, gf_mul, sbox()        gpu::State, gf_xtime, gf_mul, sbox() (aes.hpp:24-70)
+//   aes::sub_bytes ... add_round_key            gpu::sub_bytes ... add_round_key     (aes.hpp:72-78)
 //   encrypt_chunk / decrypt_chunk               gpu::encrypt_chunk / decrypt_chunk   (exec.hpp:61-65)
 //   plan_chunks / plan_decrypt_chunks           gpu::plan_chunks / ...               (chunk.hpp:37-47)
 //   pad_final / unpad_final                     gpu::pad_final / unpad_final         (chunk.hpp:49-54)
@@ -88,6 +90,62 @@ class RoundKeySchedule {
 };
 
 inline RoundKeySchedule expand_key(const Key128& key) { return RoundKeySchedule(key); }
+
+// ---- state and single-state transforms (aes.hpp:24-36, 52-78) ---------------
+// Byte i of a block sits at row i%4, column i/4.
+struct State {
+  std::array<std::uint8_t, kBlockSize> cells{};  // cells[row + 4*col]
+
+  static State from_block(const Block& b) { return State{b}; }
+  Block to_block() const { return cells; }
+  std::uint8_t& at(int row, int col) { return cells[static_cast<std::size_t>(row + 4 * col)]; }
+  std::uint8_t at(int row, int col) const { return cells[static_cast<std::size_t>(row + 4 * col)]; }
+  friend bool operator==(const State&, const State&) = default;
+};
+
+// GF(2^8) modulo x^8 + x^4 + x^3 + x + 1 (scalar helpers; the bulk path never calls them).
+constexpr std::uint8_t gf_xtime(std::uint8_t a) {
+  return static_cast<std::uint8_t>((a << 1) ^ ((a >> 7) ? 0x1b : 0x00));
+}
+constexpr std::uint8_t gf_mul(std::uint8_t a, std::uint8_t b) {
+  std::uint8_t p = 0;
+  for (; b; b >>= 1, a = gf_xtime(a))
+    if (b & 1) p ^= a;
+  return p;
+}
+
+namespace detail {
+inline std::array<std::uint8_t, 256> table(int inverse) {
+  std::array<std::uint8_t, 256> t{};
+  check(paes_cuda_sbox(inverse, t.data()));
+  return t;
+}
+inline State state_op(int op, State s, const std::uint8_t* rk = nullptr) {
+  check(paes_cuda_state_transform(op, s.cells.data(), 1, rk));
+  return s;
+}
+}  // namespace detail
+
+inline const std::array<std::uint8_t, 256>& sbox() {
+  static const auto t = detail::table(0);
+  return t;
+}
+inline const std::array<std::uint8_t, 256>& inv_sbox() {
+  static const auto t = detail::table(1);
+  return t;
+}
+
+// Each runs on the GPU (paes_cuda_state_transform); batch many states with
+// the C entry point directly.
+inline State sub_bytes(State s) { return detail::state_op(PAES_OP_SUB_BYTES, s); }
+inline State inv_sub_bytes(State s) { return detail::state_op(PAES_OP_INV_SUB_BYTES, s); }
+inline State shift_rows(State s) { return detail::state_op(PAES_OP_SHIFT_ROWS, s); }
+inline State inv_shift_rows(State s) { return detail::state_op(PAES_OP_INV_SHIFT_ROWS, s); }
+inline State mix_columns(State s) { return detail::state_op(PAES_OP_MIX_COLUMNS, s); }
+inline State inv_mix_columns(State s) { return detail::state_op(PAES_OP_INV_MIX_COLUMNS, s); }
+inline State add_round_key(State s, const RoundKey& rk) {
+  return detail::state_op(PAES_OP_ADD_ROUND_KEY, s, rk.data());
+}
 
 // ---- bulk ECB (aes.hpp:84-89): len % 16 == 0, in/out same length, may alias
 inline void encrypt_ecb(std::span<const std::uint8_t> in, std::span<std::uint8_t> out, const RoundKeySchedule& ks,

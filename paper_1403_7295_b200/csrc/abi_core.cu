@@ -7,6 +7,7 @@
 #include <algorithm>
 #include <cstring>
 #include <memory>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -82,6 +83,38 @@ int64_t paes_cuda_plan_decrypt_chunks(uint64_t cipher_len, uint32_t workers, pae
     return PAES_OK;
   });
   return rc ? rc : n;
+}
+
+int paes_cuda_sbox(int inverse, uint8_t out[256]) {
+  if (!out) return fail(PAES_EINVAL, "null buffer");
+  std::memcpy(out, inverse ? kTables.inv_sbox : kTables.sbox, 256);
+  return PAES_OK;
+}
+
+int paes_cuda_state_transform(int op, uint8_t* states, uint64_t n, const uint8_t rk16[16]) {
+  return guarded([&] {
+    if (op < PAES_OP_SUB_BYTES || op > PAES_OP_ADD_ROUND_KEY) throw std::invalid_argument("bad state op");
+    if (op == PAES_OP_ADD_ROUND_KEY && !rk16) throw std::invalid_argument("null round key");
+    if (n == 0) return PAES_OK;
+    if (!states) throw std::invalid_argument("null states");
+    if (n > (1ull << 32)) throw std::invalid_argument("too many states");
+    StateKey k{};
+    if (op == PAES_OP_ADD_ROUND_KEY) std::memcpy(k.b, rk16, 16);
+    DevCtx& d = device(device_list(1)[0]);
+    DeviceGuard g(d.id);
+    std::lock_guard<std::mutex> lk(d.mu);
+    ensure_pipeline(d, false);
+    QuiesceOnThrow quiesce{d};
+    cudaStream_t s = d.st[0];
+    std::uint8_t* dp = nullptr;
+    PAES_CK(cudaMallocAsync(reinterpret_cast<void**>(&dp), 16 * n, s));
+    PAES_CK(cudaMemcpyAsync(dp, states, 16 * n, cudaMemcpyHostToDevice, s));
+    PAES_CK(launch_state_op(op, dp, n, k, s));
+    PAES_CK(cudaMemcpyAsync(states, dp, 16 * n, cudaMemcpyDeviceToHost, s));
+    PAES_CK(cudaFreeAsync(dp, s));
+    PAES_CK(cudaStreamSynchronize(s));
+    return PAES_OK;
+  });
 }
 
 int64_t paes_cuda_pad_final(const uint8_t* raw, uint64_t len, uint8_t* out) {

@@ -5,6 +5,7 @@
 #include <atomic>
 #include <cstdint>
 
+#include "../../include/paes_cuda.h"
 #include "aes_kernels.cuh"
 #include "launch.hpp"
 
@@ -355,6 +356,56 @@ __global__ void __launch_bounds__(kThreads, 1) batch_kernel(const __grid_constan
   }
 }
 
+// ---------------------------------------------------------------- single-state transforms
+// The reference's public per-transform wrappers (aes.hpp:72-78,
+// aes.cpp:194-227) over n independent states, one thread per state, byte-wise
+// from the definitions: the KAT/test face of the cipher, not the bulk path.
+// State byte i sits at row i % 4, column i / 4 (aes.hpp:24-36).
+__device__ __forceinline__ std::uint32_t gf2(std::uint32_t a) { return ((a << 1) ^ ((a >> 7) * 0x1bu)) & 0xffu; }
+
+__device__ __forceinline__ std::uint32_t gfmul(std::uint32_t a, std::uint32_t b) {
+  std::uint32_t p = 0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    p ^= (b & 1u) ? a : 0u;
+    a = gf2(a);
+    b >>= 1;
+  }
+  return p;
+}
+
+__global__ void state_op_kernel(int op, std::uint8_t* states, unsigned long long n, StateKey rk) {
+  const unsigned long long i = static_cast<unsigned long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  std::uint8_t* p = states + 16ull * i;
+  std::uint32_t c[16], o[16];
+#pragma unroll
+  for (int j = 0; j < 16; ++j) c[j] = p[j];
+  // multipliers of one output row: {2,3,1,1} forward, {14,11,13,9} inverse
+  const std::uint32_t m0 = op == PAES_OP_MIX_COLUMNS ? 2u : 14u, m1 = op == PAES_OP_MIX_COLUMNS ? 3u : 11u;
+  const std::uint32_t m2 = op == PAES_OP_MIX_COLUMNS ? 1u : 13u, m3 = op == PAES_OP_MIX_COLUMNS ? 1u : 9u;
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {
+    const int row = j & 3, col = j >> 2;
+    switch (op) {
+      case PAES_OP_SUB_BYTES: o[j] = g_tab.sbox[c[j]]; break;
+      case PAES_OP_INV_SUB_BYTES: o[j] = g_tab.inv_sbox[c[j]]; break;
+      case PAES_OP_SHIFT_ROWS: o[j] = c[row + 4 * ((col + row) & 3)]; break;      // row r rotates left by r
+      case PAES_OP_INV_SHIFT_ROWS: o[j] = c[row + 4 * ((col - row) & 3)]; break;  // ... and back right
+      case PAES_OP_MIX_COLUMNS:
+      case PAES_OP_INV_MIX_COLUMNS: {
+        const int b = 4 * col;
+        o[j] = gfmul(c[b + row], m0) ^ gfmul(c[b + ((row + 1) & 3)], m1) ^ gfmul(c[b + ((row + 2) & 3)], m2) ^
+               gfmul(c[b + ((row + 3) & 3)], m3);
+        break;
+      }
+      default: o[j] = c[j] ^ rk.b[j]; break;  // PAES_OP_ADD_ROUND_KEY
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < 16; ++j) p[j] = static_cast<std::uint8_t>(o[j]);
+}
+
 // ---------------------------------------------------------------- utilities
 __device__ __forceinline__ unsigned long long mix64(unsigned long long z) {
   z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
@@ -456,6 +507,14 @@ cudaError_t launch_batch(bool dec, const BatchArgs& args, int sm_count, cudaStre
   const int smem = dec ? kDecSmemBytes : kEncSmemBytes;
   if (dec) batch_kernel<true, kNB><<<static_cast<unsigned>(grid), kThreads, smem, stream>>>(args);
   else batch_kernel<false, kNB><<<static_cast<unsigned>(grid), kThreads, smem, stream>>>(args);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_state_op(int op, std::uint8_t* d_states, unsigned long long n, const StateKey& rk,
+                            cudaStream_t stream) {
+  if (n == 0) return cudaSuccess;
+  state_op_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, stream>>>(op, d_states, n, rk);
   g_launches.fetch_add(1, std::memory_order_relaxed);
   return cudaGetLastError();
 }

@@ -57,6 +57,10 @@ struct KeyWords {
   std::uint32_t w[44];  // 11 round keys, in order of use by the kernel
 };
 
+struct StateKey {
+  std::uint8_t b[16];  // one round key, FIPS byte order (add_round_key)
+};
+
 struct EcbArgs {
   const std::uint8_t* in;
   std::uint8_t* out;

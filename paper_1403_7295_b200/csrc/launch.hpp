@@ -18,6 +18,9 @@ cudaError_t launch_checksum(const void* buf, unsigned long long nwords, unsigned
                             int sm_count, cudaStream_t stream);
 cudaError_t launch_mismatch(const void* a, const void* b, unsigned long long nblocks, unsigned long long* d_out,
                             int sm_count, cudaStream_t stream);
+// Single-state round transforms (PAES_OP_*) on n device-resident states.
+cudaError_t launch_state_op(int op, std::uint8_t* d_states, unsigned long long n, const StateKey& rk,
+                            cudaStream_t stream);
 unsigned long long launch_count();
 
 }  // namespace paes_b200

@@ -98,6 +98,30 @@ def expand_key(key: bytes) -> List[bytes]:
     return [rk[16 * r:16 * r + 16] for r in range(11)]
 
 
+# ---------------------------------------------------------------- single-state API
+SUB_BYTES, INV_SUB_BYTES, SHIFT_ROWS, INV_SHIFT_ROWS, MIX_COLUMNS, INV_MIX_COLUMNS, ADD_ROUND_KEY = range(7)
+
+
+def state_transform(op: int, states: bytes, rk16: bytes = None) -> bytes:
+    """The reference's per-transform wrappers (aes.hpp:72-78, aes.cpp:194-227)
+    applied on the GPU to len(states) // 16 independent states."""
+    states = bytes(states)
+    if len(states) % 16:
+        raise ValueError("states must be a whole number of 16-byte states")
+    if rk16 is not None and len(rk16) != 16:
+        raise ValueError("round key must be 16 bytes")
+    buf = (C.c_uint8 * max(len(states), 1)).from_buffer_copy(states or b"\0")
+    _raise(N.load().paes_cuda_state_transform(op, buf, len(states) // 16, rk16))
+    return bytes(buf)[: len(states)]
+
+
+def sbox(inverse: bool = False) -> bytes:
+    """sbox() / inv_sbox() (aes.hpp:69-70): the library's compile-time tables."""
+    out = (C.c_uint8 * 256)()
+    _raise(N.load().paes_cuda_sbox(int(bool(inverse)), out))
+    return bytes(out)
+
+
 # ---------------------------------------------------------------- bulk ECB
 def ecb(direction: int, data, key: bytes, ngpus: int = 0) -> bytes:
     """aes::encrypt_ecb / decrypt_ecb (aes.hpp:86-89) over host memory."""

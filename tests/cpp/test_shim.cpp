@@ -88,6 +88,25 @@ static void host_tests() {
   std::vector<std::uint8_t> inconsistent(16, 0x04);
   inconsistent[13] = 0x05;
   CHECK(throws<gpu::PaddingError>([&] { gpu::unpad_final(inconsistent); }));
+  // GF(2^8) and the S-box tables (test_aes.cpp:55-105): FIPS-197 4.2 examples,
+  // every S-box entry = affine(GF inverse), inverse table inverts it
+  CHECK(gpu::gf_xtime(0x57) == 0xae && gpu::gf_mul(0x57, 0x83) == 0xc1 && gpu::gf_mul(0x57, 0x13) == 0xfe);
+  const auto& sb = gpu::sbox();
+  const auto& isb = gpu::inv_sbox();
+  CHECK(sb[0x00] == 0x63 && sb[0x53] == 0xed);
+  for (int x = 0; x < 256; ++x) {
+    std::uint8_t inv = 0;
+    for (int y = 1; y < 256 && x; ++y)
+      if (gpu::gf_mul(static_cast<std::uint8_t>(x), static_cast<std::uint8_t>(y)) == 1) inv = static_cast<std::uint8_t>(y);
+    std::uint8_t s = 0x63;
+    for (int i = 0; i < 8; ++i) {
+      const int bit = ((inv >> i) ^ (inv >> ((i + 4) % 8)) ^ (inv >> ((i + 5) % 8)) ^ (inv >> ((i + 6) % 8)) ^
+                       (inv >> ((i + 7) % 8))) & 1;
+      s ^= static_cast<std::uint8_t>(bit << i);
+    }
+    CHECK(sb[static_cast<std::size_t>(x)] == s);
+    CHECK(isb[sb[static_cast<std::size_t>(x)]] == x);
+  }
   // argument errors before any device work
   std::vector<std::uint8_t> fifteen_b(15), out(15);
   CHECK(throws<std::invalid_argument>([&] { gpu::encrypt_ecb(fifteen_b, out, zero); }));
@@ -128,6 +147,33 @@ static void gpu_tests() {
       CHECK(std::equal(first.begin(), first.end(), c.begin()));
       CHECK(std::equal(rest.begin(), rest.end(), c.begin() + 16));
     }
+  }
+  // single-state transforms on the GPU (test_aes.cpp:136-253)
+  gpu::State st{};
+  st.at(0, 0) = 0xdb, st.at(1, 0) = 0x13, st.at(2, 0) = 0x53, st.at(3, 0) = 0x45;
+  const auto mc = gpu::mix_columns(st);
+  CHECK(mc.at(0, 0) == 0x8e && mc.at(1, 0) == 0x4d && mc.at(2, 0) == 0xa1 && mc.at(3, 0) == 0xbc);
+  gpu::State ones{};
+  for (int r = 0; r < 4; ++r) ones.at(r, 2) = 0x01;
+  CHECK(gpu::mix_columns(ones) == ones);
+  gpu::State rows{};
+  for (int r = 0; r < 4; ++r)
+    for (int col = 0; col < 4; ++col) rows.at(r, col) = static_cast<std::uint8_t>(16 * r + col);
+  const auto sr = gpu::shift_rows(rows);
+  for (int r = 0; r < 4; ++r)
+    for (int col = 0; col < 4; ++col) CHECK(sr.at(r, col) == rows.at(r, (col + r) % 4));
+  std::mt19937_64 srng(147);
+  for (int t = 0; t < 64; ++t) {
+    gpu::State s{};
+    gpu::RoundKey k{};
+    for (auto& x : s.cells) x = static_cast<std::uint8_t>(srng());
+    for (auto& x : k) x = static_cast<std::uint8_t>(srng());
+    CHECK(gpu::inv_mix_columns(gpu::mix_columns(s)) == s);
+    CHECK(gpu::inv_shift_rows(gpu::shift_rows(s)) == s);
+    CHECK(gpu::inv_sub_bytes(gpu::sub_bytes(s)) == s);
+    CHECK(gpu::add_round_key(gpu::add_round_key(s, k), k) == s);
+    const auto sub = gpu::sub_bytes(s);
+    for (std::size_t i = 0; i < 16; ++i) CHECK(sub.cells[i] == gpu::sbox()[s.cells[i]]);
   }
   // wrong key -> PaddingError (test_exec.cpp:235-247)
   std::vector<std::uint8_t> msg(100, 7);

@@ -221,3 +221,20 @@ def test_batch_descriptor_errors_before_device(paes):
     with pytest.raises(paes.PaddingError):
         paes.ecb_batch(1, 1, 1, [0], [0], [0], rk, True)
     assert paes.ecb_batch(0, 0, 0, [], [], [], b"", True) == []
+
+
+def test_sbox_tables_match_oracle(paes, orc):
+    """sbox()/inv_sbox() (aes.hpp:69-70) are the library's compile-time tables."""
+    assert paes.sbox() == orc.sbox()
+    assert paes.sbox(inverse=True) == orc.inv_sbox()
+    assert paes.sbox()[0x00] == 0x63 and paes.sbox()[0x53] == 0xED
+
+
+def test_state_transform_errors_before_device(paes):
+    with pytest.raises(ValueError):
+        paes.state_transform(paes.SUB_BYTES, bytes(15))
+    with pytest.raises(ValueError):
+        paes.state_transform(9, bytes(16))
+    with pytest.raises(ValueError):
+        paes.state_transform(paes.ADD_ROUND_KEY, bytes(16))  # no round key
+    assert paes.state_transform(paes.MIX_COLUMNS, b"") == b""
