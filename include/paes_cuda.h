@@ -195,6 +195,17 @@ typedef struct paes_job_outcome {
 int paes_cuda_run_job(const char* input_path, const char* output_path, const uint8_t key[16], uint32_t workers, int dir,
                       paes_job_outcome* outcome);
 
+/* run_worker_chunk (exec.hpp:46-59, exec.cpp:349-373): one worker's chunk,
+ * file to file.  Bytes [offset, offset + raw_len) of input_path are
+ * transformed (padded / unpadded iff is_final) and written to output_path
+ * from byte 0, through the same pipelined GPU path as run_job.  device < 0
+ * uses the first listed device.  PAES_EIO for a missing input or a short
+ * chunk (checked first, like the reference), then the chunk rules
+ * (PAES_EINVAL / PAES_EBADMSG).  The hidden worker mode of
+ * lib/paes_gpu_worker is this call. */
+int paes_cuda_worker_chunk(const char* input_path, uint64_t offset, uint64_t raw_len, int is_final, int dir,
+                           const uint8_t key[16], const char* output_path, int device);
+
 /* ---- synthetic inputs and device-side checks (bench / tests) ----------- */
 
 /* generate_sweep_file (bench.cpp:109-125) into memory: mt19937_64 seeded with

@@ -15,6 +15,8 @@
 //   plan_chunks / plan_decrypt_chunks           gpu::plan_chunks / ...               (chunk.hpp:37-47)
 //   pad_final / unpad_final                     gpu::pad_final / unpad_final         (chunk.hpp:49-54)
 //   run_job(JobSpec) + ExecStrategy             gpu::run_job (strategy "gpu")        (exec.hpp:18-51)
+//   run_worker_chunk(WorkerChunkArgs)           gpu::run_worker_chunk                (exec.hpp:46-59)
+//   assemble(plan, chunks)                      gpu::assemble                        (chunk.hpp:57-58)
 //   Error / IoError / PaddingError / WorkerError  same names, same bases           (errors.hpp:8-33)
 //
 // Error codes from the C ABI are rethrown as the reference's exception types.
@@ -248,6 +250,17 @@ inline std::size_t unpad_final(std::span<const std::uint8_t> padded) {
   return static_cast<std::size_t>(n);
 }
 
+// Plain concatenation in plan order (chunk.cpp:102-111).
+inline std::vector<std::uint8_t> assemble(const ChunkPlan& plan,
+                                          const std::vector<std::vector<std::uint8_t>>& encrypted_chunks) {
+  if (encrypted_chunks.size() != plan.chunks.size())
+    throw std::invalid_argument("assemble: chunk count does not match plan");
+  std::vector<std::uint8_t> out;
+  out.reserve(static_cast<std::size_t>(plan.output_len()));
+  for (const auto& c : encrypted_chunks) out.insert(out.end(), c.begin(), c.end());
+  return out;
+}
+
 // ---- run_job with the GPU strategy (exec.hpp:18-51, exec.cpp:340-347) ------
 enum class Direction { Encrypt, Decrypt };
 
@@ -270,6 +283,23 @@ inline JobOutcome run_job(const JobSpec& job) {
   check(paes_cuda_run_job(job.input_path.c_str(), job.output_path.c_str(), job.key.bytes.data(), job.workers,
                           job.direction == Direction::Encrypt ? PAES_ENCRYPT : PAES_DECRYPT, &o));
   return {o.bytes_in, o.bytes_out, o.seconds};
+}
+
+// One worker's chunk, file to file (exec.hpp:46-59, exec.cpp:349-373).
+struct WorkerChunkArgs {
+  std::filesystem::path input_path;
+  std::uint64_t offset = 0;
+  std::uint64_t raw_len = 0;
+  bool is_final = false;
+  Direction direction = Direction::Encrypt;
+  Key128 key;
+  std::filesystem::path out_path;
+};
+
+inline void run_worker_chunk(const WorkerChunkArgs& a, int device = -1) {
+  check(paes_cuda_worker_chunk(a.input_path.c_str(), a.offset, a.raw_len, a.is_final ? 1 : 0,
+                               a.direction == Direction::Encrypt ? PAES_ENCRYPT : PAES_DECRYPT, a.key.bytes.data(),
+                               a.out_path.c_str(), device));
 }
 
 }  // namespace paes::gpu

@@ -50,6 +50,7 @@ SIGNATURES = [
     ("paes_cuda_set_pipeline", C.c_int, [_u64, C.c_int]),
     ("paes_cuda_set_zero_copy_max", C.c_int, [_u64]),
     ("paes_cuda_expand_key", C.c_int, [_vp, _vp]),
+    ("paes_cuda_worker_chunk", C.c_int, [C.c_char_p, _u64, _u64, C.c_int, C.c_int, _vp, C.c_char_p, C.c_int]),
     ("paes_cuda_state_transform", C.c_int, [C.c_int, _vp, _u64, _vp]),
     ("paes_cuda_sbox", C.c_int, [C.c_int, _vp]),
     ("paes_cuda_plan_chunks", C.c_int64, [_u64, C.c_uint32, C.POINTER(ChunkSpec), _u64]),

@@ -105,11 +105,13 @@ void par_io(std::uint64_t n, unsigned threads, F&& f) {
 }
 
 // One GPU's shard of a file job: pread into pinned slots, H2D, kernel, D2H
-// back into the same slot, pwrite -- all slots in flight at once.  Returns
-// the output bytes written (decrypt final: unpadded).
-std::uint64_t file_shard(DevCtx& d, const Range& r, int in_fd, int out_fd, std::uint8_t* out_map, std::uint64_t off,
-                         const KeyWords& kw, const std::string& in_path, const std::string& out_path,
-                         unsigned io_threads) {
+// back into the same slot, pwrite -- all slots in flight at once.  Input
+// bytes [in_off, in_off + r.in_len) land at out_off in the output (run_job:
+// equal offsets; a worker chunk: its own file from 0).  Returns the output
+// bytes written (decrypt final: unpadded).
+std::uint64_t file_shard(DevCtx& d, const Range& r, int in_fd, int out_fd, std::uint8_t* out_map,
+                         std::uint64_t in_off, std::uint64_t out_off, const KeyWords& kw, const std::string& in_path,
+                         const std::string& out_path, unsigned io_threads) {
   DeviceGuard g(d.id);
   ensure_pipeline(d, true);
   const int S = static_cast<int>(d.st.size());
@@ -158,14 +160,14 @@ std::uint64_t file_shard(DevCtx& d, const Range& r, int in_fd, int out_fd, std::
     const bool last = k + 1 == npieces;
     std::uint8_t* slot = d.hbuf[s];
     par_io(len, io_threads,
-           [&](std::uint64_t o, std::uint64_t n) { pread_all(in_fd, slot + o, n, off + poff + o, in_path); });
+           [&](std::uint64_t o, std::uint64_t n) { pread_all(in_fd, slot + o, n, in_off + poff + o, in_path); });
     EcbArgs a = make_args(r, d.dbuf[s], d.dbuf[s], len, last, kw, d.m_status);
     if (len) PAES_CK(cudaMemcpyAsync(d.dbuf[s], d.hbuf[s], len, cudaMemcpyHostToDevice, d.st[s]));
     PAES_CK(launch_ecb(r.dec, a, d.sm_count, d.st[s]));
     const std::uint64_t olen = a.nblocks * 16;
     if (olen) PAES_CK(cudaMemcpyAsync(d.hbuf[s], d.dbuf[s], olen, cudaMemcpyDeviceToHost, d.st[s]));
     PAES_CK(cudaEventRecord(d.ev[s], d.st[s]));
-    writer[s] = std::thread(write_slot, s, off + poff, olen);
+    writer[s] = std::thread(write_slot, s, out_off + poff, olen);
     out_total = poff + olen;
   }
   for (int s = 0; s < S; ++s) join_slot(s);
@@ -231,7 +233,7 @@ extern "C" int paes_cuda_run_job(const char* input_path, const char* output_path
         const unsigned io = g_io_threads_per_shard
                                 ? g_io_threads_per_shard
                                 : std::clamp<unsigned>(hw / static_cast<unsigned>(plan.size()), 1u, 8u);
-        produced[i] = file_shard(d, r, in.fd, out.fd, map.p, c.offset, kw, in_path, tmp, io);
+        produced[i] = file_shard(d, r, in.fd, out.fd, map.p, c.offset, c.offset, kw, in_path, tmp, io);
       } catch (const CudaFail& e) {
         failures[i] = e.msg;
       } catch (const IoFail& e) {
@@ -269,4 +271,67 @@ extern "C" int paes_cuda_run_job(const char* input_path, const char* output_path
   });
   if (rc != PAES_OK && !tmp.empty()) ::unlink(tmp.c_str());  // no partial output (exec.cpp:86-91)
   return rc;
+}
+// run_worker_chunk (exec.hpp:46-59, exec.cpp:349-373): one worker's chunk,
+// file to file -- bytes [offset, offset + raw_len) of the input, padded or
+// unpadded iff final, written to out_path from 0.  The same pipelined shard
+// as run_job (pinned ring, parallel pread, writer threads into a mapping).
+// Errors in the reference's order: IoError for the input first, then the
+// chunk-transform rules (invalid_argument / PaddingError).
+extern "C" int paes_cuda_worker_chunk(const char* input_path, uint64_t offset, uint64_t raw_len, int is_final,
+                                      int dir, const uint8_t key[16], const char* output_path, int device) {
+  return guarded([&] {
+    try {
+      if (!input_path || !output_path || !key) throw std::invalid_argument("null argument");
+      if (dir != PAES_ENCRYPT && dir != PAES_DECRYPT) throw std::invalid_argument("bad dir");
+      const std::string in_path(input_path), out_path(output_path);
+      Fd in;
+      in.fd = ::open(input_path, O_RDONLY);
+      if (in.fd < 0) throw IoFail{"cannot open input: " + in_path};
+      struct stat stt {};
+      if (::fstat(in.fd, &stt) != 0) throw IoFail{"cannot stat input: " + in_path};
+      const std::uint64_t size = static_cast<std::uint64_t>(stt.st_size);
+      if (offset > size || raw_len > size - offset)
+        throw IoFail{"short read of chunk [" + std::to_string(offset) + ", +" + std::to_string(raw_len) +
+                     "): " + in_path};
+      const bool dec = dir == PAES_DECRYPT;
+      const bool final = is_final != 0;
+      if (!final && raw_len % 16 != 0) throw std::invalid_argument("non-final chunk length must be a multiple of 16");
+      if (dec && raw_len % 16 != 0) throw std::invalid_argument("decrypt: length must be a multiple of 16");
+      if (dec && final && raw_len == 0) throw PaddingError("unpad: length must be a non-zero multiple of 16");
+      Range r;
+      r.dec = dec;
+      r.in_len = raw_len;
+      r.pad = !dec && final;
+      r.check_pad = dec && final;
+      std::uint8_t rk[176];
+      expand_key(key, rk);
+      const KeyWords kw = dec ? dec_key_words(rk) : enc_key_words(rk);
+      const int dev = device >= 0 ? device : device_list(1)[0];
+      Fd out;
+      out.fd = ::open(output_path, O_RDWR | O_CREAT | O_TRUNC, 0644);
+      if (out.fd < 0) throw IoFail{"cannot open output: " + out_path};
+      const std::uint64_t cap = r.pad ? (raw_len / 16 + 1) * 16 : raw_len;
+      Map map;
+      if (cap && ::ftruncate(out.fd, static_cast<off_t>(cap)) == 0) {
+        void* p = ::mmap(nullptr, cap, PROT_READ | PROT_WRITE, MAP_SHARED, out.fd, 0);
+        if (p != MAP_FAILED) {
+          map.p = static_cast<std::uint8_t*>(p);
+          map.n = cap;
+        }
+      }
+      std::uint64_t produced = 0;
+      if (cap) {
+        DevCtx& d = rt::device(dev);
+        std::lock_guard<std::mutex> lk(d.mu);
+        const unsigned io = g_io_threads_per_shard ? g_io_threads_per_shard
+                                                   : std::clamp<unsigned>(std::thread::hardware_concurrency(), 1u, 8u);
+        produced = file_shard(d, r, in.fd, out.fd, map.p, offset, 0, kw, in_path, out_path, io);
+      }
+      if (::ftruncate(out.fd, static_cast<off_t>(produced)) != 0) throw IoFail{"truncate failed: " + out_path};
+      return PAES_OK;
+    } catch (const IoFail& e) {
+      return fail(PAES_EIO, e.msg);
+    }
+  });
 }

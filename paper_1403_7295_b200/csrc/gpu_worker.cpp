@@ -9,21 +9,18 @@
 // exec.cpp:349-373), so the reference's UNMODIFIED process strategy
 // (run_process_isolated, exec.cpp:272-338) drives B200s when its
 // JobSpec::worker_exe points here: one process per chunk, one GPU each.
-// The chunk is transformed by the library's host-pointer path
-// (paes_cuda_chunk).  Device: --device, else PAES_WORKER_DEVICE, else the
+// The chunk goes through paes_cuda_worker_chunk: the library's pipelined
+// file shard (parallel pread -> pinned ring -> kernel -> mapped output).  Device: --device, else PAES_WORKER_DEVICE, else the
 // chunk's index (offset / len) modulo the visible devices.
 //
 // Exit codes (paes_main.cpp:316-325): 0 ok, 2 invalid argument, 1 anything else.
-#include <fcntl.h>
 #include <unistd.h>
 
-#include <cerrno>
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <string>
-#include <vector>
 
 #include "paes_cuda.h"
 
@@ -32,17 +29,6 @@ namespace {
 int usage(const char* msg) {
   std::fprintf(stderr, "worker: %s\n", msg);
   return 2;
-}
-
-bool read_all(int fd, std::uint8_t* p, std::uint64_t n, std::uint64_t off) {
-  std::uint64_t got = 0;
-  while (got < n) {
-    const ssize_t r = ::pread(fd, p + got, n - got, static_cast<off_t>(off + got));
-    if (r < 0 && errno == EINTR) continue;
-    if (r <= 0) return false;
-    got += static_cast<std::uint64_t>(r);
-  }
-  return true;
 }
 
 }  // namespace
@@ -99,36 +85,10 @@ int main(int argc, char** argv) {
     return 1;
   }
 
-  const int fd = ::open(in.c_str(), O_RDONLY);
-  if (fd < 0) {
-    std::fprintf(stderr, "worker: cannot open input: %s\n", in.c_str());
-    return 1;
-  }
-  std::vector<std::uint8_t> raw(len), res(len + 16);
-  const bool ok = read_all(fd, raw.data(), len, offset);
-  ::close(fd);
-  if (!ok) {
-    std::fprintf(stderr, "worker: short read of chunk [%llu, +%llu): %s\n", static_cast<unsigned long long>(offset),
-                 static_cast<unsigned long long>(len), in.c_str());
-    return 1;
-  }
-  std::uint8_t rk[176];
-  paes_cuda_expand_key(key, rk);
-  std::uint64_t olen = 0;
-  const int rc = paes_cuda_chunk(d, raw.data(), len, final_flag, rk, res.data(), &olen, 1);
+  const int rc = paes_cuda_worker_chunk(in.c_str(), offset, len, final_flag, d, key, out.c_str(), device);
   if (rc != PAES_OK) {
     std::fprintf(stderr, "worker: %s\n", paes_cuda_last_error());
     return rc == PAES_EINVAL ? 2 : 1;
-  }
-  FILE* f = std::fopen(out.c_str(), "wb");
-  if (!f) {
-    std::fprintf(stderr, "worker: cannot open output: %s\n", out.c_str());
-    return 1;
-  }
-  const bool wrote = olen == 0 || std::fwrite(res.data(), 1, olen, f) == olen;
-  if (std::fclose(f) != 0 || !wrote) {
-    std::fprintf(stderr, "worker: write failed: %s\n", out.c_str());
-    return 1;
   }
   return 0;
 }

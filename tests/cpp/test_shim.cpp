@@ -107,6 +107,14 @@ static void host_tests() {
     CHECK(sb[static_cast<std::size_t>(x)] == s);
     CHECK(isb[sb[static_cast<std::size_t>(x)]] == x);
   }
+  // assemble (chunk.cpp:102-111): concatenation in plan order, count must match
+  const auto plan3 = gpu::plan_chunks(100, 3);
+  CHECK(gpu::assemble(plan3, {{1, 2}, {3}, {4, 5, 6}}) == std::vector<std::uint8_t>({1, 2, 3, 4, 5, 6}));
+  CHECK(throws<std::invalid_argument>([&] { gpu::assemble(plan3, {{1}}); }));
+  // run_worker_chunk: the input is checked first, IoError like exec.cpp:350-366
+  CHECK(throws<gpu::IoError>([] {
+    gpu::run_worker_chunk({"/nonexistent/paes_in", 0, 16, true, gpu::Direction::Encrypt, gpu::Key128{}, "/tmp/x"});
+  }));
   // argument errors before any device work
   std::vector<std::uint8_t> fifteen_b(15), out(15);
   CHECK(throws<std::invalid_argument>([&] { gpu::encrypt_ecb(fifteen_b, out, zero); }));
@@ -199,6 +207,40 @@ static void gpu_tests() {
   std::ifstream in(dir / "mb.dec", std::ios::binary);
   std::vector<std::uint8_t> got((std::istreambuf_iterator<char>(in)), std::istreambuf_iterator<char>());
   CHECK(got == big);
+  // run_worker_chunk over a 4-way plan, assembled == the whole-file ciphertext
+  // (test_exec.cpp:291-312), then decrypted chunk by chunk
+  const auto wplan = gpu::plan_chunks(big.size(), 4);
+  std::vector<std::vector<std::uint8_t>> parts;
+  for (std::size_t i = 0; i < wplan.chunks.size(); ++i) {
+    const auto& c = wplan.chunks[i];
+    const auto part = dir / ("part" + std::to_string(i));
+    gpu::run_worker_chunk({dir / "mb.bin", c.offset, c.raw_len, c.is_final, gpu::Direction::Encrypt, job.key, part});
+    std::ifstream pf(part, std::ios::binary);
+    parts.emplace_back((std::istreambuf_iterator<char>(pf)), std::istreambuf_iterator<char>());
+    CHECK(parts.back().size() == c.padded_len);
+  }
+  const auto whole = gpu::assemble(wplan, parts);
+  CHECK(whole == gpu::encrypt_chunk(big, true, gpu::RoundKeySchedule(job.key)));
+  const auto dplan = gpu::plan_decrypt_chunks(whole.size(), 3);
+  std::vector<std::uint8_t> plain;
+  for (std::size_t i = 0; i < dplan.chunks.size(); ++i) {
+    const auto& c = dplan.chunks[i];
+    const auto part = dir / ("plain" + std::to_string(i));
+    gpu::run_worker_chunk({dir / "mb.enc", c.offset, c.raw_len, c.is_final, gpu::Direction::Decrypt, job.key, part});
+    std::ifstream pf(part, std::ios::binary);
+    plain.insert(plain.end(), std::istreambuf_iterator<char>(pf), std::istreambuf_iterator<char>());
+  }
+  CHECK(plain == big);
+  gpu::Key128 wrong_key = job.key;
+  wrong_key.bytes[3] ^= 0x40;
+  const auto& last = dplan.chunks.back();
+  CHECK(throws<gpu::PaddingError>([&] {
+    gpu::run_worker_chunk(
+        {dir / "mb.enc", last.offset, last.raw_len, true, gpu::Direction::Decrypt, wrong_key, dir / "bad.part"});
+  }));
+  CHECK(throws<gpu::IoError>([&] {  // chunk past the end of the file
+    gpu::run_worker_chunk({dir / "mb.enc", whole.size() - 16, 32, true, gpu::Direction::Decrypt, job.key, dir / "x"});
+  }));
   gpu::JobSpec wrong = dec;
   wrong.output_path = dir / "bad.dec";
   wrong.key.bytes[5] ^= 0x01;
