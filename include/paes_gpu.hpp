@@ -25,9 +25,11 @@
 #include <array>
 #include <cstdint>
 #include <filesystem>
+#include <optional>
 #include <span>
 #include <stdexcept>
 #include <string>
+#include <string_view>
 #include <vector>
 
 #include "paes_cuda.h"
@@ -264,12 +266,36 @@ inline std::vector<std::uint8_t> assemble(const ChunkPlan& plan,
 // ---- run_job with the GPU strategy (exec.hpp:18-51, exec.cpp:340-347) ------
 enum class Direction { Encrypt, Decrypt };
 
+// The reference's strategies plus the GPU one (exec.hpp:18, exec.cpp:24-38).
+// Only Gpu runs here: the CPU strategies are the reference's own code.
+enum class ExecStrategy { Sequential, Threaded, ProcessIsolated, Gpu };
+
+constexpr std::string_view to_string(ExecStrategy s) {
+  switch (s) {
+    case ExecStrategy::Sequential: return "sequential";
+    case ExecStrategy::Threaded: return "threads";
+    case ExecStrategy::ProcessIsolated: return "processes";
+    case ExecStrategy::Gpu: return "gpu";
+  }
+  return "gpu";
+}
+
+constexpr std::optional<ExecStrategy> strategy_from_string(std::string_view name) {
+  if (name == "sequential") return ExecStrategy::Sequential;
+  if (name == "threads") return ExecStrategy::Threaded;
+  if (name == "processes") return ExecStrategy::ProcessIsolated;
+  if (name == "gpu") return ExecStrategy::Gpu;
+  return std::nullopt;
+}
+
 struct JobSpec {
   std::filesystem::path input_path;
   std::filesystem::path output_path;
   Key128 key;
   unsigned workers = 1;  // GPUs; 0 = all visible
   Direction direction = Direction::Encrypt;
+  ExecStrategy strategy = ExecStrategy::Gpu;
+  std::filesystem::path worker_exe;  // unused by the gpu strategy (kept for source compatibility)
 };
 
 struct JobOutcome {
@@ -279,6 +305,9 @@ struct JobOutcome {
 };
 
 inline JobOutcome run_job(const JobSpec& job) {
+  if (job.strategy != ExecStrategy::Gpu)
+    throw std::invalid_argument("strategy '" + std::string(to_string(job.strategy)) +
+                                "' runs on the CPU in the reference library; paes::gpu runs only 'gpu'");
   paes_job_outcome o{};
   check(paes_cuda_run_job(job.input_path.c_str(), job.output_path.c_str(), job.key.bytes.data(), job.workers,
                           job.direction == Direction::Encrypt ? PAES_ENCRYPT : PAES_DECRYPT, &o));

@@ -107,6 +107,15 @@ static void host_tests() {
     CHECK(sb[static_cast<std::size_t>(x)] == s);
     CHECK(isb[sb[static_cast<std::size_t>(x)]] == x);
   }
+  // strategy names (exec.cpp:24-38) + "gpu"; CPU strategies are refused loudly
+  CHECK(gpu::to_string(gpu::ExecStrategy::Threaded) == "threads");
+  CHECK(gpu::strategy_from_string("processes") == gpu::ExecStrategy::ProcessIsolated);
+  CHECK(gpu::strategy_from_string("gpu") == gpu::ExecStrategy::Gpu);
+  CHECK(!gpu::strategy_from_string("cuda").has_value());
+  CHECK(throws<std::invalid_argument>([] {
+    gpu::JobSpec j{"/tmp/a", "/tmp/b", gpu::Key128{}, 1, gpu::Direction::Encrypt, gpu::ExecStrategy::Threaded, {}};
+    gpu::run_job(j);
+  }));
   // assemble (chunk.cpp:102-111): concatenation in plan order, count must match
   const auto plan3 = gpu::plan_chunks(100, 3);
   CHECK(gpu::assemble(plan3, {{1, 2}, {3}, {4, 5, 6}}) == std::vector<std::uint8_t>({1, 2, 3, 4, 5, 6}));
