@@ -284,6 +284,13 @@ def set_pipeline(chunk_bytes: int = 0, streams: int = 0) -> None:
     _raise(N.load().paes_cuda_set_pipeline(chunk_bytes, streams))
 
 
+def csv_header() -> str:
+    """The bench report's CSV header (paes_module.cpp:151, report.hpp:12-13)."""
+    from .report import CSV_HEADER
+
+    return CSV_HEADER
+
+
 def set_zero_copy_max(nbytes: int) -> None:
     """Pinned host ranges up to ``nbytes`` run as one zero-copy kernel on the
     caller's buffers (0 = always use the copy-engine ring)."""

@@ -7,6 +7,9 @@ from paper_1403_7295_b200 import report
 
 def test_csv_header_is_the_references(golden):
     assert report.CSV_HEADER == golden["csv_header"]
+    from paper_1403_7295_b200 import paes
+
+    assert paes.csv_header() == golden["csv_header"]  # the _paes mirror's entry (paes_module.cpp:151)
 
 
 def test_measure_cell_with_scripted_samples():
