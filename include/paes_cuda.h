@@ -85,7 +85,10 @@ int paes_cuda_set_pipeline(uint64_t chunk_bytes, int streams);
 /* Pinned host ranges up to this many bytes (per device shard) skip the copy
  * ring: one kernel reads and writes the caller's pinned buffers over PCIe
  * through their UVA aliases.  0 disables.  Default 128 MiB
- * (profiles/r01_zero_copy_probe.json). */
+ * (profiles/r01_zero_copy_probe.json).  cudaHostRegister'ed buffers (default
+ * flags) are mapped into the GPU lazily: the first call on a freshly
+ * registered buffer is slow (2 GB/s), later calls are not; register with
+ * cudaHostRegisterMapped, or set 0, to avoid it. */
 int paes_cuda_set_zero_copy_max(uint64_t bytes);
 
 /* ---- host-side rules (no GPU needed) ------------------------------------ */
