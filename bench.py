@@ -274,6 +274,36 @@ def workload_config(args, impl: str = "b200"):
 
 
 # --------------------------------------------------------------------- B200 arm
+def _cpulist(text: str):
+    cpus = set()
+    for part in text.strip().split(","):
+        if "-" in part:
+            a, b = part.split("-")
+            cpus.update(range(int(a), int(b) + 1))
+        elif part:
+            cpus.add(int(part))
+    return cpus
+
+
+def bind_to_gpu_numa(torch, dev: int) -> str:
+    """Pin this rank's host threads to the CPUs of its GPU's NUMA node, so the
+    pinned e2e buffers (first-touch) and the ring's host copies stay local to
+    the GPU's PCIe root -- with 8 ranks the host DRAM traffic is the e2e
+    limit.  Only under torchrun (N > 1): at N = 1 the CPU baseline must keep
+    every host core."""
+    try:
+        p = torch.cuda.get_device_properties(dev)
+        bdf = f"{p.pci_domain_id:04x}:{p.pci_bus_id:02x}:{p.pci_device_id:02x}.0"
+        node = int(open(f"/sys/bus/pci/devices/{bdf}/numa_node").read())
+        if node < 0:
+            return f"unbound ({bdf}: no NUMA node)"
+        cpus = _cpulist(open(f"/sys/devices/system/node/node{node}/cpulist").read())
+        os.sched_setaffinity(0, cpus)
+        return f"node{node} ({len(cpus)} cpus, GPU {bdf})"
+    except Exception as e:  # best effort: never fail the bench over placement
+        return f"unbound ({e})"
+
+
 def run_b200(args, dist: Dist):
     import torch
 
@@ -282,6 +312,7 @@ def run_b200(args, dist: Dist):
     dev = 0 if os.environ.get("PAES_BENCH_SHARED_DEVICE") == "1" else dist.local
     torch.cuda.set_device(dev)
     paes.set_devices([dev])
+    numa = bind_to_gpu_numa(torch, dev) if dist.world > 1 else "unbound (N = 1: all host cores)"
     N = dist.world
     shard = rank_shard(args.total_bytes, N, dist.rank, paes.plan_chunks)
     off, n, is_final = shard["offset"], shard["raw_len"], shard["is_final"]
@@ -424,6 +455,7 @@ def run_b200(args, dist: Dist):
     e2e = None
     if not args.no_e2e and n:
         e2e = run_e2e(args, dist, paes, torch, pt, n, out_n, is_final, rk, dev)
+        e2e["numa"] = numa
 
     result = {
         "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": N, "steps": args.steps,
