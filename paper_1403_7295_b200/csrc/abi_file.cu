@@ -246,7 +246,11 @@ extern "C" int paes_cuda_run_job(const char* input_path, const char* output_path
       work(0);
     } else {
       std::vector<std::thread> pool;
-      for (std::size_t i = 0; i < plan.size(); ++i) pool.emplace_back(work, i);
+      for (std::size_t i = 0; i < plan.size(); ++i)
+        pool.emplace_back([&, i] {
+          bind_thread_to_device_numa(devs[i]);
+          work(i);
+        });
       for (auto& t : pool) t.join();
     }
     std::ostringstream failed;

@@ -10,11 +10,14 @@
 #include <atomic>
 #include <cuda_runtime.h>
 #include <fcntl.h>
+#include <pthread.h>
+#include <sched.h>
 #include <sys/mman.h>
 #include <sys/stat.h>
 #include <unistd.h>
 
 #include <algorithm>
+#include <cctype>
 #include <cerrno>
 #include <chrono>
 #include <cstdio>
@@ -51,6 +54,53 @@ int visible_devices() {
     return 0;
   }
   return n;
+}
+
+// CPUs of a device's NUMA node (from sysfs via its PCI address); empty when
+// the platform reports none.  Cached per device.
+const cpu_set_t* device_numa_cpus(int dev) {
+  static std::mutex mu;
+  static cpu_set_t sets[kMaxDev];
+  static int state[kMaxDev];  // 0 unknown, 1 have set, 2 none
+  if (dev < 0 || dev >= kMaxDev) return nullptr;
+  std::lock_guard<std::mutex> lk(mu);
+  if (state[dev] == 0) {
+    state[dev] = 2;
+    char bdf[32] = {0};
+    if (cudaDeviceGetPCIBusId(bdf, sizeof bdf, dev) != cudaSuccess) {
+      cudaGetLastError();
+      return nullptr;
+    }
+    std::string id(bdf);
+    for (auto& ch : id) ch = static_cast<char>(std::tolower(static_cast<unsigned char>(ch)));
+    int node = -1;
+    if (FILE* f = std::fopen(("/sys/bus/pci/devices/" + id + "/numa_node").c_str(), "r")) {
+      if (std::fscanf(f, "%d", &node) != 1) node = -1;
+      std::fclose(f);
+    }
+    if (node < 0) return nullptr;
+    char list[4096] = {0};
+    if (FILE* f = std::fopen(("/sys/devices/system/node/node" + std::to_string(node) + "/cpulist").c_str(), "r")) {
+      if (!std::fgets(list, sizeof list, f)) list[0] = 0;
+      std::fclose(f);
+    }
+    CPU_ZERO(&sets[dev]);
+    int ncpu = 0;
+    char* save = nullptr;
+    for (char* tok = strtok_r(list, ",\n", &save); tok; tok = strtok_r(nullptr, ",\n", &save)) {
+      int a = -1, b = -1;
+      const int k = std::sscanf(tok, "%d-%d", &a, &b);
+      if (k < 1) continue;
+      if (k == 1) b = a;
+      for (int c = a; c <= b && c < CPU_SETSIZE; ++c, ++ncpu) CPU_SET(c, &sets[dev]);
+    }
+    if (ncpu) state[dev] = 1;
+  }
+  return state[dev] == 1 ? &sets[dev] : nullptr;
+}
+
+void bind_thread_to_device_numa(int dev) {
+  if (const cpu_set_t* s = device_numa_cpus(dev)) pthread_setaffinity_np(pthread_self(), sizeof(cpu_set_t), s);
 }
 
 // Lazily initialise a device: kernel attributes, status words.
@@ -388,9 +438,13 @@ int host_transform(int dir, const std::uint8_t* in, std::uint64_t len, bool is_f
   };
   if (plan.size() == 1) {
     work(0);
-  } else {
+  } else {  // one library-owned thread per shard, on its GPU's NUMA node
     std::vector<std::thread> pool;
-    for (std::size_t i = 0; i < plan.size(); ++i) pool.emplace_back(work, i);
+    for (std::size_t i = 0; i < plan.size(); ++i)
+      pool.emplace_back([&, i] {
+        bind_thread_to_device_numa(devs[i]);
+        work(i);
+      });
     for (auto& t : pool) t.join();
   }
   for (std::size_t i = 0; i < plan.size(); ++i)

@@ -93,6 +93,9 @@ int visible_devices();
 DevCtx& device(int id);
 // Pipeline buffers (device ring, optional pinned host ring); d.mu held.
 void ensure_pipeline(DevCtx& d, bool need_host);
+// Pins the calling library-owned thread (and the threads it spawns) to the
+// CPUs of the device's NUMA node; a no-op where sysfs reports no node.
+void bind_thread_to_device_numa(int dev);
 // Drains a device's ring streams when its scope is left by an exception: the
 // copies and kernels already queued still target the caller's buffers and the
 // ring's slots, so returning an error code before they finish would hand the
