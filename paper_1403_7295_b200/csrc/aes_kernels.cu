@@ -28,14 +28,27 @@ constexpr int kThreads = PAES_THREADS;  // one persistent CTA per SM (smem-limit
 // word index w:  region = w >> 14, row x = (w >> 6) & 255, table-in-region
 // t = (w >> 5) & 1, lane = w & 31.  Four consecutive words (4 lanes) share a
 // value, so the fill is one 16-byte store per 4 words.
+// Two phases: the CTA first copies the 1 KiB base table (+ InvS) into a
+// scratch area with a handful of coalesced loads, then every thread expands
+// its share from that copy (broadcast LDS, 2 rows per warp per pass).  Reading
+// the base table straight from global memory in the fill put every thread of
+// all 148 SMs on the same few L2 lines: ~2-3 us of contention per launch
+// (profiles/r01_small_latency.json: staging 4.1 us with 1 CTA, 6-7 with 148).
 // The trip count is a compile-time constant (kernels launch with kThreads), so
-// the loop unrolls and all of a thread's table reads are in flight together
-// instead of one L2 round trip per 16-byte store.
+// the fill loop unrolls.
 template <bool DEC>
 __device__ __forceinline__ void stage_tables(std::uint32_t* sm) {
-  const std::uint32_t* base = DEC ? g_tab.td0 : g_tab.te0;
-  constexpr int nvec = (DEC ? kDecSmemBytes : kEncSmemBytes) / 16;
+  constexpr int kTabBytes = DEC ? kDecSmemBytes : kEncSmemBytes;
+  constexpr int nvec = kTabBytes / 16;
   static_assert(nvec % kThreads == 0, "staging assumes whole passes");
+  static_assert(kThreads >= 256 + 64, "one scratch word per thread");
+  // the CTA's single copy of the base table (+ InvS): 8-10 coalesced requests
+  std::uint32_t* base = sm + kTabBytes / 4;
+  const int tid = static_cast<int>(threadIdx.x);
+  if (tid < 256) base[tid] = (DEC ? g_tab.td0 : g_tab.te0)[tid];
+  else if (DEC && tid < 256 + 64) base[tid] = reinterpret_cast<const std::uint32_t*>(g_tab.inv_sbox)[tid - 256];
+  __syncthreads();
+  const std::uint8_t* inv_sbox = reinterpret_cast<const std::uint8_t*>(base + 256);
 #pragma unroll
   for (int it = 0; it < nvec / kThreads; ++it) {
     const int i = it * kThreads + static_cast<int>(threadIdx.x);
@@ -49,7 +62,7 @@ __device__ __forceinline__ void stage_tables(std::uint32_t* sm) {
       const int rot = (region * 2 + t) * 8;
       v = (v << rot) | (rot ? (v >> (32 - rot)) : 0u);
     } else {
-      v = t == 0 ? static_cast<std::uint32_t>(g_tab.inv_sbox[x]) * 0x01010101u : 0u;
+      v = t == 0 ? static_cast<std::uint32_t>(inv_sbox[x]) * 0x01010101u : 0u;
     }
     reinterpret_cast<uint4*>(sm)[i] = make_uint4(v, v, v, v);
   }
@@ -210,7 +223,9 @@ __global__ void __launch_bounds__(kThreads, 1) ecb_kernel(const __grid_constant_
   // the ragged loop so the pad check always runs
   const unsigned long long full_tiles = (a.check_pad ? a.nfull - 1 : a.nfull) / kTile;
   const unsigned long long wpc = blockDim.x / 32;
-  unsigned long long tile = blockIdx.x * wpc + threadIdx.x / 32;
+  // tiles interleave across CTAs (tile t -> CTA t mod grid), so a short input
+  // spreads over many SMs instead of queueing on one SM's lookup pipe
+  unsigned long long tile = static_cast<unsigned long long>(threadIdx.x / 32) * gridDim.x + blockIdx.x;
   const unsigned long long tstride = gridDim.x * wpc;
 
   // steady state: whole tiles of whole input blocks, no per-block checks.
@@ -280,7 +295,8 @@ __global__ void __launch_bounds__(kThreads, 1) batch_kernel(const __grid_constan
   const std::uint32_t lane4 = lane * 4;
   constexpr unsigned long long kTile = 32ull * NB;
   const unsigned long long nwarps = static_cast<unsigned long long>(gridDim.x) * (blockDim.x / 32);
-  const unsigned long long warp = static_cast<unsigned long long>(blockIdx.x) * (blockDim.x / 32) + threadIdx.x / 32;
+  // warps numbered CTA-minor, so consecutive tile ranges land on different SMs
+  const unsigned long long warp = static_cast<unsigned long long>(threadIdx.x / 32) * gridDim.x + blockIdx.x;
   const unsigned long long t_begin = a.total_tiles * warp / nwarps;
   const unsigned long long t_end = a.total_tiles * (warp + 1) / nwarps;
   if (t_begin >= t_end) return;
@@ -470,22 +486,22 @@ constexpr int kNB = PAES_NB;  // blocks per thread per warp tile
 
 cudaError_t prepare_kernels() {
   cudaError_t e;
-  if ((e = set_smem(ecb_kernel<false, kNB, true>, kEncSmemBytes))) return e;
-  if ((e = set_smem(ecb_kernel<false, kNB, false>, kEncSmemBytes))) return e;
-  if ((e = set_smem(ecb_kernel<true, kNB, true>, kDecSmemBytes))) return e;
-  if ((e = set_smem(ecb_kernel<true, kNB, false>, kDecSmemBytes))) return e;
-  if ((e = set_smem(batch_kernel<false, kNB>, kEncSmemBytes))) return e;
-  if ((e = set_smem(batch_kernel<true, kNB>, kDecSmemBytes))) return e;
+  if ((e = set_smem(ecb_kernel<false, kNB, true>, kEncLaunchSmem))) return e;
+  if ((e = set_smem(ecb_kernel<false, kNB, false>, kEncLaunchSmem))) return e;
+  if ((e = set_smem(ecb_kernel<true, kNB, true>, kDecLaunchSmem))) return e;
+  if ((e = set_smem(ecb_kernel<true, kNB, false>, kDecLaunchSmem))) return e;
+  if ((e = set_smem(batch_kernel<false, kNB>, kEncLaunchSmem))) return e;
+  if ((e = set_smem(batch_kernel<true, kNB>, kDecLaunchSmem))) return e;
   return cudaSuccess;
 }
 
 cudaError_t launch_ecb(bool dec, const EcbArgs& args, int sm_count, cudaStream_t stream) {
   if (args.nblocks == 0) return cudaSuccess;
-  const unsigned long long per_cta = static_cast<unsigned long long>(kThreads) * kNB;
-  unsigned long long grid = (args.nblocks + per_cta - 1) / per_cta;
-  if (grid > static_cast<unsigned long long>(sm_count)) grid = sm_count;
+  // one CTA per SM, or one per warp tile when there are fewer tiles than SMs
+  const unsigned long long ntiles = (args.nblocks + 32ull * kNB - 1) / (32ull * kNB);
+  const unsigned long long grid = ntiles < static_cast<unsigned long long>(sm_count) ? ntiles : sm_count;
   const bool aligned = ((reinterpret_cast<std::uintptr_t>(args.in) | reinterpret_cast<std::uintptr_t>(args.out)) & 15) == 0;
-  const int smem = dec ? kDecSmemBytes : kEncSmemBytes;
+  const int smem = dec ? kDecLaunchSmem : kEncLaunchSmem;
   if (dec) {
     if (aligned) ecb_kernel<true, kNB, true><<<static_cast<unsigned>(grid), kThreads, smem, stream>>>(args);
     else ecb_kernel<true, kNB, false><<<static_cast<unsigned>(grid), kThreads, smem, stream>>>(args);
@@ -501,10 +517,10 @@ unsigned batch_tile_blocks() { return 32u * kNB; }
 
 cudaError_t launch_batch(bool dec, const BatchArgs& args, int sm_count, cudaStream_t stream) {
   if (args.total_tiles == 0) return cudaSuccess;
-  const unsigned long long per_cta = kThreads / 32;  // warp tiles per CTA per wave
-  unsigned long long grid = (args.total_tiles + per_cta - 1) / per_cta;
-  if (grid > static_cast<unsigned long long>(sm_count)) grid = sm_count;
-  const int smem = dec ? kDecSmemBytes : kEncSmemBytes;
+  // one CTA per SM, or one per warp tile when there are fewer tiles than SMs
+  const unsigned long long grid =
+      args.total_tiles < static_cast<unsigned long long>(sm_count) ? args.total_tiles : sm_count;
+  const int smem = dec ? kDecLaunchSmem : kEncLaunchSmem;
   if (dec) batch_kernel<true, kNB><<<static_cast<unsigned>(grid), kThreads, smem, stream>>>(args);
   else batch_kernel<false, kNB><<<static_cast<unsigned>(grid), kThreads, smem, stream>>>(args);
   g_launches.fetch_add(1, std::memory_order_relaxed);

@@ -45,6 +45,12 @@ namespace paes_b200 {
 constexpr int kTableRegionBytes = 65536;  // 256 rows x 256 bytes
 constexpr int kEncSmemBytes = 2 * kTableRegionBytes;
 constexpr int kDecSmemBytes = 3 * kTableRegionBytes;
+// After the tables: the CTA's one copy of Te0 (or Td0 + InvS) that the
+// replica fill reads, loaded with a few coalesced requests per CTA instead of
+// every thread of every SM hammering the same L2 lines.
+constexpr int kScratchBytes = 2048;
+constexpr int kEncLaunchSmem = kEncSmemBytes + kScratchBytes;
+constexpr int kDecLaunchSmem = kDecSmemBytes + kScratchBytes;
 
 // offsets of table k inside the smem window
 constexpr int kT0 = 0;
