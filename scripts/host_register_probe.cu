@@ -2,7 +2,7 @@
 // staged?  Times cudaHostRegister / cudaHostUnregister of touched malloc'd
 // memory, and the transform of the registered range through paes_cuda_chunk,
 // against the staged pageable path.  One JSON line.
-// Build: see scripts/small_latency.cu.
+// Build: scripts/build_probes.sh
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>

@@ -5,7 +5,7 @@
 //   hybrid   : per piece, H2D by copy engine, then the kernel writes its output
 //              straight into the pinned host buffer; pieces double-buffered
 // GB/s = input bytes / wall time.  One JSON line.
-// Build: see scripts/small_latency.cu.
+// Build: scripts/build_probes.sh
 #include <chrono>
 #include <cstdio>
 #include <cstring>

@@ -1,7 +1,7 @@
 // Zero-copy on cudaHostRegister'ed malloc memory vs cudaHostAlloc memory:
 // flags reported by cudaHostGetFlags, and per-call throughput of repeated
 // transforms (zero-copy route vs copy ring) on the same registered buffer.
-// Build: see scripts/small_latency.cu.
+// Build: scripts/build_probes.sh
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>

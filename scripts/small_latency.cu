@@ -1,7 +1,6 @@
 // Per-call latency of small transforms through the C ABI, against the floor
 // of an empty kernel launch + stream sync and a mapped-memory round trip.
-// Build: nvcc -gencode arch=compute_100a,code=sm_100a -O2 -I include scripts/small_latency.cu
-//        -L paper_1403_7295_b200/lib -lpaes_cuda -Xlinker -rpath=$PWD/paper_1403_7295_b200/lib -o /tmp/small_latency
+// Build: scripts/build_probes.sh
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>

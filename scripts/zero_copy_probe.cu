@@ -2,7 +2,7 @@
 // with zero-copy disabled) against one zero-copy kernel that reads and writes the host buffers over
 // PCIe through their UVA device pointers (paes_cuda_chunk_device on host
 // pointers).  Prints one JSON line; GB/s = input bytes / wall time per call.
-// Build: see scripts/small_latency.cu.
+// Build: scripts/build_probes.sh
 #include <chrono>
 #include <cstdio>
 #include <cstring>
