@@ -84,6 +84,33 @@ class _InBuf:
             self.ptr = C.addressof(arr)
 
 
+_new_bytes_api = C.pythonapi.PyBytes_FromStringAndSize
+_new_bytes_api.restype = C.py_object
+_new_bytes_api.argtypes = [C.c_void_p, C.c_ssize_t]
+
+
+class _OutBytes:
+    """A fresh, not-yet-shared bytes object the library writes into directly,
+    so a result reaches Python with no extra copy (the reference returns
+    py::bytes too).  Sizes below 16 fall back to a ctypes buffer: CPython
+    shares its empty bytes object."""
+
+    def __init__(self, n: int):
+        self.n = n
+        if n >= BLOCK:
+            self.obj = _new_bytes_api(None, n)  # uninitialised, refcount 1, hash not yet cached
+            self.ptr = C.cast(C.c_char_p(self.obj), C.c_void_p).value
+        else:
+            self.obj = C.create_string_buffer(max(n, 1))
+            self.ptr = C.addressof(self.obj)
+
+    def result(self, m: int) -> bytes:
+        if not isinstance(self.obj, bytes):
+            return C.string_at(self.ptr, m)
+        # an unpadded decrypt is 1-16 bytes short of the buffer: one slice copy
+        return self.obj if m == self.n else self.obj[:m]
+
+
 def round_keys(key: bytes) -> bytes:
     """176-byte expanded schedule (RoundKeySchedule, aes.cpp:151-180)."""
     key = _as_key(key)
@@ -127,9 +154,9 @@ def ecb(direction: int, data, key: bytes, ngpus: int = 0) -> bytes:
     """aes::encrypt_ecb / decrypt_ecb (aes.hpp:86-89) over host memory."""
     rk = round_keys(key)
     src = _InBuf(data)
-    out = C.create_string_buffer(max(src.n, 1))
-    _raise(N.load().paes_cuda_ecb(direction, src.ptr, out, src.n, rk, ngpus))
-    return out.raw[: src.n]
+    out = _OutBytes(src.n)
+    _raise(N.load().paes_cuda_ecb(direction, src.ptr, out.ptr, src.n, rk, ngpus))
+    return out.result(src.n)
 
 
 def encrypt_ecb(data, key: bytes, ngpus: int = 0) -> bytes:
@@ -158,11 +185,12 @@ def chunk(direction: int, data, is_final: bool, key: bytes, ngpus: int = 0) -> b
     """encrypt_chunk / decrypt_chunk (exec.hpp:61-65) over host memory."""
     rk = round_keys(key)
     src = _InBuf(data)
-    cap = src.n + (BLOCK if (direction == ENCRYPT and is_final) else 0)
-    out = C.create_string_buffer(max(cap, 1))
+    cap = (src.n // BLOCK + 1) * BLOCK if (direction == ENCRYPT and is_final) else src.n
+    out = _OutBytes(cap)
     olen = C.c_uint64()
-    _raise(N.load().paes_cuda_chunk(direction, src.ptr, src.n, int(bool(is_final)), rk, out, C.byref(olen), ngpus))
-    return out.raw[: olen.value]
+    _raise(N.load().paes_cuda_chunk(direction, src.ptr, src.n, int(bool(is_final)), rk, out.ptr, C.byref(olen),
+                                    ngpus))
+    return out.result(olen.value)
 
 
 def encrypt_chunk(data, is_final: bool, key: bytes, ngpus: int = 0) -> bytes:
