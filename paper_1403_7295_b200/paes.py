@@ -185,11 +185,26 @@ def chunk(direction: int, data, is_final: bool, key: bytes, ngpus: int = 0) -> b
     """encrypt_chunk / decrypt_chunk (exec.hpp:61-65) over host memory."""
     rk = round_keys(key)
     src = _InBuf(data)
+    L = N.load()
+    if direction == DECRYPT and is_final and src.n >= BLOCK and src.n % BLOCK == 0:
+        # Size the result exactly, so it needs no trimming copy: decrypt the
+        # trailer block first (GPU), apply unpad_final's rule to it, then
+        # decrypt the leading n-16 bytes as a non-final chunk straight into
+        # the result and append the trailer's unpadded part.
+        last = C.create_string_buffer(BLOCK)
+        _raise(L.paes_cuda_ecb(DECRYPT, src.ptr + src.n - BLOCK, last, BLOCK, rk, 1))
+        keep = L.paes_cuda_unpad_final(last, BLOCK)
+        _raise(keep)  # PaddingError on a malformed trailer, as the in-kernel check would raise
+        head = src.n - BLOCK
+        out = _OutBytes(head + keep)
+        olen = C.c_uint64()
+        _raise(L.paes_cuda_chunk(DECRYPT, src.ptr, head, 0, rk, out.ptr, C.byref(olen), ngpus))
+        C.memmove(out.ptr + head, last, keep)
+        return out.result(head + keep)
     cap = (src.n // BLOCK + 1) * BLOCK if (direction == ENCRYPT and is_final) else src.n
     out = _OutBytes(cap)
     olen = C.c_uint64()
-    _raise(N.load().paes_cuda_chunk(direction, src.ptr, src.n, int(bool(is_final)), rk, out.ptr, C.byref(olen),
-                                    ngpus))
+    _raise(L.paes_cuda_chunk(direction, src.ptr, src.n, int(bool(is_final)), rk, out.ptr, C.byref(olen), ngpus))
     return out.result(olen.value)
 
 
