@@ -46,6 +46,19 @@ struct Map {
   }
 };
 
+// Size the output to `cap` and map it shared (plain pwrite if the file system
+// refuses mmap).  Its pages are allocated by the writer threads' own faults,
+// in parallel: preallocating with fallocate on a side thread was measured
+// slower (scripts/ab_file_variants.py, profiles/r01_file_prealloc_ab.json).
+void open_output(int fd, std::uint64_t cap, Map& map) {
+  if (!cap || ::ftruncate(fd, static_cast<off_t>(cap)) != 0) return;
+  void* p = ::mmap(nullptr, cap, PROT_READ | PROT_WRITE, MAP_SHARED, fd, 0);
+  if (p != MAP_FAILED) {
+    map.p = static_cast<std::uint8_t*>(p);
+    map.n = cap;
+  }
+}
+
 void pread_all(int fd, std::uint8_t* p, std::uint64_t n, std::uint64_t off, const std::string& path) {
   std::uint64_t got = 0;
   while (got < n) {
@@ -210,13 +223,7 @@ extern "C" int paes_cuda_run_job(const char* input_path, const char* output_path
     // a decrypt's unpad); plain pwrite if the file system refuses mmap.
     const std::uint64_t cap = dec ? len : (len / 16 + 1) * 16;
     Map map;
-    if (cap && ::ftruncate(out.fd, static_cast<off_t>(cap)) == 0) {
-      void* p = ::mmap(nullptr, cap, PROT_READ | PROT_WRITE, MAP_SHARED, out.fd, 0);
-      if (p != MAP_FAILED) {
-        map.p = static_cast<std::uint8_t*>(p);
-        map.n = cap;
-      }
-    }
+    open_output(out.fd, cap, map);
     std::vector<std::uint64_t> produced(plan.size(), 0);
     std::vector<std::string> failures(plan.size());
     auto work = [&](std::size_t i) {
@@ -317,13 +324,7 @@ extern "C" int paes_cuda_worker_chunk(const char* input_path, uint64_t offset, u
       if (out.fd < 0) throw IoFail{"cannot open output: " + out_path};
       const std::uint64_t cap = r.pad ? (raw_len / 16 + 1) * 16 : raw_len;
       Map map;
-      if (cap && ::ftruncate(out.fd, static_cast<off_t>(cap)) == 0) {
-        void* p = ::mmap(nullptr, cap, PROT_READ | PROT_WRITE, MAP_SHARED, out.fd, 0);
-        if (p != MAP_FAILED) {
-          map.p = static_cast<std::uint8_t*>(p);
-          map.n = cap;
-        }
-      }
+      open_output(out.fd, cap, map);
       std::uint64_t produced = 0;
       if (cap) {
         DevCtx& d = rt::device(dev);
