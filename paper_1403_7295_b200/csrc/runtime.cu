@@ -287,6 +287,24 @@ std::uint64_t run_zero_copy(DevCtx& d, const Range& r, const void* din, void* do
   return olen;
 }
 
+cudaError_t copy_h2d_aligned(void* dev, const void* host, std::uint64_t n, cudaStream_t s) {
+  const std::uint64_t head = (4096 - reinterpret_cast<std::uintptr_t>(host) % 4096) % 4096;
+  if (head == 0 || head >= n) return cudaMemcpyAsync(dev, host, n, cudaMemcpyHostToDevice, s);
+  const cudaError_t e = cudaMemcpyAsync(dev, host, head, cudaMemcpyHostToDevice, s);
+  if (e != cudaSuccess) return e;
+  return cudaMemcpyAsync(static_cast<std::uint8_t*>(dev) + head, static_cast<const std::uint8_t*>(host) + head, n - head,
+                         cudaMemcpyHostToDevice, s);
+}
+
+cudaError_t copy_d2h_aligned(void* host, const void* dev, std::uint64_t n, cudaStream_t s) {
+  const std::uint64_t head = (4096 - reinterpret_cast<std::uintptr_t>(host) % 4096) % 4096;
+  if (head == 0 || head >= n) return cudaMemcpyAsync(host, dev, n, cudaMemcpyDeviceToHost, s);
+  const cudaError_t e = cudaMemcpyAsync(host, dev, head, cudaMemcpyDeviceToHost, s);
+  if (e != cudaSuccess) return e;
+  return cudaMemcpyAsync(static_cast<std::uint8_t*>(host) + head, static_cast<const std::uint8_t*>(dev) + head, n - head,
+                         cudaMemcpyDeviceToHost, s);
+}
+
 // memcpy split over host threads (a single core moves ~10 GB/s; the pinned
 // slots are fed at PCIe rate).
 void par_copy(std::uint8_t* dst, const std::uint8_t* src, std::uint64_t n) {
@@ -383,10 +401,10 @@ std::uint64_t run_host_range(DevCtx& d, const Range& r, const std::uint8_t* in, 
     const std::uint64_t len = std::min<std::uint64_t>(C, r.in_len - off);
     const bool last = k + 1 == npieces;
     EcbArgs a = make_args(r, d.dbuf[s], d.dbuf[s], len, last, kw, d.m_status);
-    if (len) PAES_CK(cudaMemcpyAsync(d.dbuf[s], in + off, len, cudaMemcpyHostToDevice, d.st[s]));
+    if (len) PAES_CK(copy_h2d_aligned(d.dbuf[s], in + off, len, d.st[s]));
     PAES_CK(launch_ecb(r.dec, a, d.sm_count, d.st[s]));
     const std::uint64_t olen = a.nblocks * 16;
-    if (olen) PAES_CK(cudaMemcpyAsync(out + off, d.dbuf[s], olen, cudaMemcpyDeviceToHost, d.st[s]));
+    if (olen) PAES_CK(copy_d2h_aligned(out + off, d.dbuf[s], olen, d.st[s]));
     out_total = off + olen;
   }
   for (auto s : d.st) PAES_CK(cudaStreamSynchronize(s));

@@ -76,7 +76,7 @@ struct DevCtx {
   std::vector<std::uint8_t*> dbuf;  // chunk + 16 bytes each
   std::vector<std::uint8_t*> hbuf;  // pinned staging for the file path
   std::vector<std::uint8_t*> obuf;  // second device ring (batch output spans), chunk + 16 each, lazy
-  std::vector<std::uint8_t*> dsc;   // per-stream batch descriptor images, lazy, grow-only
+  std::vector<std::uint8_t*> dsc;   // [0]: the host batch's device descriptor image (all groups), lazy, grow-only
   std::vector<std::size_t> dsc_cap;
   std::vector<cudaEvent_t> ev;
   std::uint64_t chunk = 0;
@@ -96,6 +96,14 @@ void ensure_pipeline(DevCtx& d, bool need_host);
 // Pins the calling library-owned thread (and the threads it spawns) to the
 // CPUs of the device's NUMA node; a no-op where sysfs reports no node.
 void bind_thread_to_device_numa(int dev);
+// Pinned host <-> device copies whose bulk runs on 4 KiB-aligned host
+// addresses: a head copy up to the next page boundary, then the rest.  With
+// H2D and D2H in flight together (the ring), copies that start mid-page cost
+// ~9 % of the PCIe rate (scripts/host_align_probe.py: 43.0 vs 47.2 GB/s);
+// alone they do not (scripts/copy_align_probe.cu).
+cudaError_t copy_h2d_aligned(void* dev, const void* host, std::uint64_t n, cudaStream_t s);
+cudaError_t copy_d2h_aligned(void* host, const void* dev, std::uint64_t n, cudaStream_t s);
+
 // Drains a device's ring streams when its scope is left by an exception: the
 // copies and kernels already queued still target the caller's buffers and the
 // ring's slots, so returning an error code before they finish would hand the
