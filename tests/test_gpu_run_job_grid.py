@@ -1,8 +1,10 @@
-"""test_exec.cpp:64-137 restated for the "gpu" strategy: run_job output is
-byte-identical to the reference's own sequential run_job across sizes x
-worker counts, and decrypt inverts encrypt across worker pairings.  W GPU
-workers are emulated by listing device 0 W times (same sharder, threads and
-per-shard rings; shards serialise on the device lock)."""
+"""test_exec.cpp:64-137 and acceptance.cpp:86-175 restated for the "gpu"
+strategy: run_job output is byte-identical to the reference's own sequential
+run_job across sizes x worker counts {1,2,3,4,8,16,32}, decrypt inverts
+encrypt across worker pairings, and 200 files round-trip against every
+reference strategy.  W GPU workers are emulated by listing device 0 W times
+(same sharder, threads and per-shard rings; shards serialise on the device
+lock)."""
 import os
 import random
 
@@ -15,7 +17,7 @@ SIZES = [0, 1, 15, 16, 17, 31, 32, 1000, 65536, 1_000_007]
 
 @pytest.fixture
 def eight_workers(paes):
-    paes.set_devices([0] * 8)
+    paes.set_devices([0] * 32)
     yield
     paes.set_devices([])
 
@@ -29,7 +31,7 @@ def test_gpu_run_job_equals_reference_sequential(paes, gpu, ref, eight_workers, 
         rc, _, _, _ = ref.run_job(str(src), str(tmp_path / "ref.enc"), key, 1, 0, 0)
         assert rc == 0
         expected = (tmp_path / "ref.enc").read_bytes()
-        for workers in (1, 2, 3, 8):
+        for workers in (1, 2, 3, 4, 8, 16, 32):
             out = tmp_path / "gpu.enc"
             o = paes.encrypt_file(str(src), str(out), key, workers=workers)
             assert o["bytes_in"] == size and o["bytes_out"] == len(expected)
@@ -55,3 +57,27 @@ def test_decrypt_inverts_encrypt_across_pairings(paes, gpu, ref, eight_workers, 
     with pytest.raises(paes.WorkerError, match="chunk 3"):
         paes.decrypt_file(str(tmp_path / "c.enc"), str(tmp_path / "bad.bin"), bad, workers=4)
     assert not (tmp_path / "bad.bin").exists()
+
+
+def test_acceptance_roundtrip_200_files(paes, gpu, ref, eight_workers, tmp_path):
+    """acceptance.cpp:120-175: 200 files (edge sizes, then log-uniform up to
+    1 MB), workers 1 + i % 4.  The gpu ciphertext equals the reference's
+    sequential and threaded ones, and decrypts back under the gpu strategy and
+    under the reference's threaded strategy."""
+    rnd = random.Random(0x0CE4C1E5)
+    src, enc, back = tmp_path / "plain.bin", tmp_path / "c.enc", tmp_path / "p.bin"
+    for i in range(200):
+        size = [0, 1, 15, 16, 17, 31, 32, 1_000_000][i] if i < 8 else int(2.0 ** (rnd.randrange(10000) / 10000 * 20))
+        data = rnd.randbytes(size)
+        src.write_bytes(data)
+        key = rnd.randbytes(16)
+        w = 1 + i % 4
+        paes.encrypt_file(str(src), str(enc), key, workers=w)
+        ct = enc.read_bytes()
+        for strategy, rw in ((0, 1), (1, w)):  # sequential, threads
+            rc, _, _, _ = ref.run_job(str(src), str(tmp_path / "r.enc"), key, rw, strategy, 0)
+            assert rc == 0 and (tmp_path / "r.enc").read_bytes() == ct, (i, size, strategy)
+        paes.decrypt_file(str(enc), str(back), key, workers=w)
+        assert back.read_bytes() == data, (i, size)
+        rc, _, _, _ = ref.run_job(str(enc), str(back), key, w, 1, 1)
+        assert rc == 0 and back.read_bytes() == data, (i, size)
