@@ -36,20 +36,24 @@ def _stale() -> bool:
     return any(os.path.getmtime(p) > t for p in deps)
 
 
-def build(force: bool = False, verbose: bool = False, defines=(), out_lib: str | None = None) -> str:
-    """Compile + link.  `defines` (e.g. ["PAES_NB=4"]) and `out_lib` are for
-    tuning variants (scripts/tune_variants.py); the product uses the defaults."""
+def build(force: bool = False, verbose: bool = False, defines=(), out_lib: str | None = None,
+          host_flags=()) -> str:
+    """Compile + link.  `defines` (e.g. ["PAES_NB=4"]), `host_flags` (e.g.
+    ["-fsanitize=thread"], host compiler + link) and `out_lib` are for variants
+    (scripts/tune_variants.py, scripts/tsan_stress.sh); the product uses the
+    defaults."""
     lib = out_lib or LIB
     if not force and out_lib is None and not _stale():
         return LIB
     lib_dir = os.path.dirname(lib)
     os.makedirs(lib_dir, exist_ok=True)
     dflags = ["-D" + d for d in defines]
+    hflags = ["-Xcompiler", ",".join(host_flags)] if host_flags else []
     from concurrent.futures import ThreadPoolExecutor
 
     def compile_one(src):
         obj = os.path.join(lib_dir, src + ".o")
-        cmd = [NVCC] + CCBIN + ARCH + FLAGS + dflags + ["-c", os.path.join(CSRC, src), "-o", obj]
+        cmd = [NVCC] + CCBIN + ARCH + FLAGS + dflags + hflags + ["-c", os.path.join(CSRC, src), "-o", obj]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError("nvcc failed for %s:\n%s%s" % (src, r.stdout, r.stderr))
@@ -60,7 +64,7 @@ def build(force: bool = False, verbose: bool = False, defines=(), out_lib: str |
     with ThreadPoolExecutor(len(SOURCES)) as ex:
         objs = list(ex.map(compile_one, SOURCES))
     tmp = lib + ".tmp"
-    cmd = [NVCC] + CCBIN + ARCH + ["-shared", "-o", tmp] + objs + ["-lpthread"]
+    cmd = [NVCC] + CCBIN + ARCH + hflags + ["-shared", "-o", tmp] + objs + ["-lpthread"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError("link failed:\n%s%s" % (r.stdout, r.stderr))
