@@ -2,7 +2,7 @@
 mixed operations (pageable / pinned / zero-copy / device-pointer transforms,
 host batches, file jobs, state transforms, runtime reconfiguration) under
 concurrency, every result checked by round trip.  The same driver runs under
-ThreadSanitizer via scripts/tsan_stress.sh (profiles/r01_tsan_stress.log)."""
+ThreadSanitizer via scripts/sanitizer_stress.sh (profiles/r01_tsan_stress.log)."""
 from __future__ import annotations
 
 import os
