@@ -82,7 +82,16 @@ class ClockSampler:
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
     def __init__(self, device: int):
-        self.device = device
+        # nvidia-smi's --id is its own (PCI-ordered) index; the CUDA ordinal can
+        # differ (CUDA_VISIBLE_DEVICES, device order), so pass the PCI bus id
+        self.device = str(device)
+        try:
+            import torch
+
+            p = torch.cuda.get_device_properties(device)
+            self.device = f"{p.pci_domain_id:08x}:{p.pci_bus_id:02x}:{p.pci_device_id:02x}.0"
+        except Exception:  # no torch / no CUDA: keep the ordinal
+            pass
         self.proc = None
         self.out = None
 
