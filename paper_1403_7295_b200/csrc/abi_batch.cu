@@ -139,6 +139,53 @@ std::uint8_t* staging(std::size_t bytes, int device) {
   return st.p;
 }
 
+// Per-thread device image for one-shot batches, reused call to call.  A
+// stream-ordered malloc/free per call let the pool trim at every sync point,
+// and some calls then took twice as long (scripts/oneshot_batch_probe.py).
+// Reuse is guarded by an event recorded after the kernel that read the image:
+// the next call's upload waits on it in stream order.
+struct DevImage {
+  int device = -1;
+  std::uint8_t* p = nullptr;
+  std::size_t cap = 0;
+  cudaEvent_t done = nullptr;
+  void release() {
+    if (done) {
+      cudaEventSynchronize(done);
+      cudaEventDestroy(done);
+    }
+    if (p) {
+      int prev = -1;
+      cudaGetDevice(&prev);
+      cudaSetDevice(device);
+      cudaFree(p);
+      if (prev >= 0) cudaSetDevice(prev);
+    }
+    p = nullptr, cap = 0, done = nullptr;
+  }
+  ~DevImage() { release(); }
+};
+thread_local DevImage t_dimg;
+
+std::uint8_t* device_image(std::size_t bytes, int device, cudaStream_t s) {
+  DevImage& di = t_dimg;
+  if (di.device != device) {
+    di.release();
+    di.device = device;
+  }
+  if (!di.done) PAES_CK(cudaEventCreateWithFlags(&di.done, cudaEventDisableTiming));
+  if (di.cap < bytes) {
+    PAES_CK(cudaEventSynchronize(di.done));
+    if (di.p) PAES_CK(cudaFree(di.p));
+    di.p = nullptr;
+    di.cap = 0;
+    PAES_CK(cudaMalloc(reinterpret_cast<void**>(&di.p), bytes));
+    di.cap = bytes;
+  }
+  PAES_CK(cudaStreamWaitEvent(s, di.done, 0));  // the previous call's kernel has finished reading it
+  return di.p;
+}
+
 }  // namespace
 
 struct paes_batch_plan {
@@ -163,19 +210,18 @@ int paes_cuda_ecb_batch(int dir, const void* d_in, void* d_out, const uint64_t* 
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     std::uint8_t* host = staging(b.total_bytes, device_id);
     write_batch_image(b, in_off, out_off, rks, host);
-    std::uint8_t* dd = nullptr;
-    PAES_CK(cudaMallocAsync(reinterpret_cast<void**>(&dd), b.total_bytes, s));
+    std::uint8_t* dd = device_image(b.total_bytes, device_id, s);
     PAES_CK(cudaMemcpyAsync(dd, host, b.image_bytes, cudaMemcpyHostToDevice, s));
     PAES_CK(cudaEventRecord(t_stage.ev, s));
     PAES_CK(launch_batch(b.dec, batch_args(b, d_in, d_out, dd), d.sm_count, s));
     if (b.check) {
       auto* st = reinterpret_cast<std::uint32_t*>(host + b.status_off);
       PAES_CK(cudaMemcpyAsync(st, dd + b.status_off, 4ull * n, cudaMemcpyDeviceToHost, s));
-      PAES_CK(cudaFreeAsync(dd, s));
+      PAES_CK(cudaEventRecord(t_dimg.done, s));
       PAES_CK(cudaStreamSynchronize(s));
       finish_lengths(b, st, out_lens);
     } else {
-      PAES_CK(cudaFreeAsync(dd, s));
+      PAES_CK(cudaEventRecord(t_dimg.done, s));
       finish_lengths(b, nullptr, out_lens);
     }
     return PAES_OK;

@@ -331,6 +331,13 @@ __global__ void __launch_bounds__(kThreads, 1) batch_kernel(const __grid_constan
     }
   };
   enter(m);
+  // register double buffer as in ecb_kernel: while a whole tile is computed
+  // the next tile of the same message (when whole too) is already loading.
+  // Encrypt only: measured +0.7 % for encrypt, -0.5 % for decrypt, whose
+  // higher register use leaves the loads sunk too far into the rounds.
+  constexpr bool kPrefetch = !DEC;
+  Block4 nxt[NB];
+  bool have_nxt = false;
   for (unsigned long long tile = t_begin; tile < t_end; ++tile) {
     if (tile >= next_first) {
       do {
@@ -345,13 +352,26 @@ __global__ void __launch_bounds__(kThreads, 1) batch_kernel(const __grid_constan
     if (t0 + kTile + a.check_pad <= msg.nfull) {
       // whole input blocks only: no per-block checks
       const unsigned long long lb = t0 + lane;
+      if (kPrefetch && have_nxt) {
 #pragma unroll
-      for (int j = 0; j < NB; ++j) s[j] = load_block<true>(src + 16ull * (lb + 32ull * j));
+        for (int j = 0; j < NB; ++j) s[j] = nxt[j];
+      } else {
+#pragma unroll
+        for (int j = 0; j < NB; ++j) s[j] = load_block<true>(src + 16ull * (lb + 32ull * j));
+      }
+      if constexpr (kPrefetch) {
+        have_nxt = tile + 1 < t_end && tile + 1 < next_first && t0 + 2 * kTile + a.check_pad <= msg.nfull;
+        if (have_nxt) {
+#pragma unroll
+          for (int j = 0; j < NB; ++j) nxt[j] = load_block<true>(src + 16ull * (lb + kTile + 32ull * j));
+        }
+      }
       cipher<DEC, NB>(s, kw, smb, lane4);
 #pragma unroll
       for (int j = 0; j < NB; ++j) store_block<true>(dst + 16ull * (lb + 32ull * j), s[j]);
     } else {
       // the message's last tile: partial blocks, pad block, trailer check
+      have_nxt = false;
 #pragma unroll
       for (int j = 0; j < NB; ++j) {
         const unsigned long long lb = t0 + lane + 32ull * j;
