@@ -140,6 +140,18 @@ class ClockSampler:
                 "samples": len(rows), "samples_under_load": len(loaded), "power_w_max": pmax}
 
 
+def clocks_suspect(clocks: dict) -> bool:
+    """Timing rules: a region that saw thermal / HW slowdown, or SM clocks far
+    below max with no reason given (a leftover clock lock), is measured once
+    more.  sw_power_cap is kept and noted."""
+    bad = {"hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"}
+    if bad & set(clocks.get("reasons") or []):
+        return True
+    if clocks.get("sm_mhz") and clocks.get("sm_max_mhz") and not clocks.get("reasons"):
+        return clocks["sm_mhz"] < 0.8 * clocks["sm_max_mhz"]
+    return False
+
+
 # --------------------------------------------------------------------- dist
 class Dist:
     """One process per GPU (torchrun env).  NCCL on GPUs; gloo for the CPU tests.
@@ -380,13 +392,7 @@ def run_b200(args, dist: Dist):
                 clk.summary(peaks.get("sm_max_mhz", 1965.0)))
 
     launches, elapsed_ms, kern_ms, clocks = timed_region()
-    # timing rules: a region that saw thermal / HW slowdown, or SM clocks far
-    # below max with no reason (a leftover clock lock), is measured once more
-    bad = {"hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"}
-    suspect = bool(bad & set(clocks.get("reasons") or []))
-    if clocks.get("sm_mhz") and clocks.get("sm_max_mhz") and not clocks.get("reasons"):
-        suspect |= clocks["sm_mhz"] < 0.8 * clocks["sm_max_mhz"]
-    if int(dist.reduce(int(suspect), "max")):
+    if int(dist.reduce(int(clocks_suspect(clocks)), "max")):
         first = dict(clocks)
         launches, elapsed_ms, kern_ms, clocks = timed_region()
         clocks["remeasured_after"] = first
