@@ -154,6 +154,21 @@ __device__ __forceinline__ void cipher(Block4 (&s)[NB], const K& kw, const char*
 }
 
 // ---------------------------------------------------------------- global I/O
+// 16 bytes starting `sh` (0..15) bytes into the 32-byte concatenation lo:hi
+// (warp-uniform switch on the word offset, then a funnel shift).
+__device__ __forceinline__ Block4 bytes_at(const Block4& lo, const Block4& hi, unsigned sh) {
+  const unsigned bs = (sh & 3) * 8;
+  std::uint32_t w0, w1, w2, w3, w4;
+  switch (sh >> 2) {
+    case 0: w0 = lo.x, w1 = lo.y, w2 = lo.z, w3 = lo.w, w4 = hi.x; break;
+    case 1: w0 = lo.y, w1 = lo.z, w2 = lo.w, w3 = hi.x, w4 = hi.y; break;
+    case 2: w0 = lo.z, w1 = lo.w, w2 = hi.x, w3 = hi.y, w4 = hi.z; break;
+    default: w0 = lo.w, w1 = hi.x, w2 = hi.y, w3 = hi.z, w4 = hi.w; break;
+  }
+  return Block4{__funnelshift_r(w0, w1, bs), __funnelshift_r(w1, w2, bs), __funnelshift_r(w2, w3, bs),
+                __funnelshift_r(w3, w4, bs)};
+}
+
 template <bool ALIGNED>
 __device__ __forceinline__ Block4 load_block(const std::uint8_t* p) {
   if (ALIGNED) {
@@ -171,17 +186,7 @@ __device__ __forceinline__ Block4 load_block(const std::uint8_t* p) {
     const uint4 v0 = __ldcs(q);
     if (sh == 0) return Block4{v0.x, v0.y, v0.z, v0.w};
     const uint4 v1 = __ldcs(q + 1);
-    const unsigned bs = (sh & 3) * 8;
-    std::uint32_t w0, w1, w2, w3, w4;
-    switch (sh >> 2) {
-      case 0: w0 = v0.x, w1 = v0.y, w2 = v0.z, w3 = v0.w, w4 = v1.x; break;
-      case 1: w0 = v0.y, w1 = v0.z, w2 = v0.w, w3 = v1.x, w4 = v1.y; break;
-      case 2: w0 = v0.z, w1 = v0.w, w2 = v1.x, w3 = v1.y, w4 = v1.z; break;
-      default: w0 = v0.w, w1 = v1.x, w2 = v1.y, w3 = v1.z, w4 = v1.w; break;
-    }
-    // bs == 0 (4-byte aligned): the words are already in place
-    return Block4{__funnelshift_r(w0, w1, bs), __funnelshift_r(w1, w2, bs), __funnelshift_r(w2, w3, bs),
-                  __funnelshift_r(w3, w4, bs)};
+    return bytes_at(Block4{v0.x, v0.y, v0.z, v0.w}, Block4{v1.x, v1.y, v1.z, v1.w}, sh);
   }
 }
 
@@ -200,6 +205,36 @@ __device__ __forceinline__ void store_block(std::uint8_t* p, const Block4& b) {
 #pragma unroll
     for (int c = 0; c < 16; ++c) p[c] = static_cast<std::uint8_t>(w[c >> 2] >> (8 * (c & 3)));
   }
+}
+
+// A full warp row (32 consecutive blocks, lane l's at row + 16 l) stored at an
+// address that is not 4-byte aligned: lane l writes the aligned 16-byte chunk
+// l+1 from its own tail and lane l+1's head (one shuffle per word), lanes 0
+// and 31 write the two partial end chunks byte by byte.  Every write covers
+// only this row's bytes, so in-place operation and neighbouring rows are safe.
+// 1 STG.128 + 4 SHFL per lane instead of 16 byte stores.
+__device__ __forceinline__ void store_row_unaligned(std::uint8_t* row, const Block4& v, std::uint32_t lane) {
+  const std::uintptr_t a = reinterpret_cast<std::uintptr_t>(row);
+  const unsigned m = static_cast<unsigned>(a & 15);  // 1..15
+  std::uint8_t* c = reinterpret_cast<std::uint8_t*>(a - m);
+  const Block4 n{__shfl_down_sync(0xffffffffu, v.x, 1), __shfl_down_sync(0xffffffffu, v.y, 1),
+                 __shfl_down_sync(0xffffffffu, v.z, 1), __shfl_down_sync(0xffffffffu, v.w, 1)};
+  if (lane < 31) {
+    const Block4 k = bytes_at(v, n, 16 - m);
+    __stcs(reinterpret_cast<uint4*>(c + 16ull * (lane + 1)), make_uint4(k.x, k.y, k.z, k.w));
+  }
+  // the two partial end chunks, one byte per lane: lanes 0..15-m write chunk
+  // 0's bytes m..15 from lane 0's block, lanes 16..15+m write chunk 32's
+  // bytes 0..m-1 from lane 31's block (broadcast by shuffle)
+  const bool head = lane < 16 - m, tail = lane >= 16 && lane < 16 + m;
+  const unsigned src = tail ? 31u : 0u;
+  const Block4 e{__shfl_sync(0xffffffffu, v.x, src), __shfl_sync(0xffffffffu, v.y, src),
+                 __shfl_sync(0xffffffffu, v.z, src), __shfl_sync(0xffffffffu, v.w, src)};
+  const unsigned b = head ? lane : (lane - 16) + (16 - m);  // byte index within the source block
+  const std::uint32_t wv = b < 4 ? e.x : b < 8 ? e.y : b < 12 ? e.z : e.w;
+  const std::uint8_t byte = static_cast<std::uint8_t>(wv >> (8 * (b & 3)));
+  if (head) c[m + lane] = byte;
+  else if (tail) c[512 + (lane - 16)] = byte;
 }
 
 // PKCS#7 always-pad block: tail bytes then k = 16 - tail_len copies of k.
@@ -257,11 +292,18 @@ __global__ void __launch_bounds__(kThreads, 1) ecb_kernel(const __grid_constant_
   // launches, all stall on the same load latency together.  The first tile's
   // loads are issued before the tables are staged, so their HBM latency hides
   // behind the staging (this is most of a small launch's duration).
+  // Full tiles keep all 32 lanes active, so an output that is not even
+  // 4-byte aligned is written by whole rows (store_row_unaligned).  Measured
+  // on 1 GiB (scripts/unaligned_probe.py): per-lane double-chunk loads + word
+  // stores at offsets 4/8 (753 GB/s) and + row stores at odd offsets (684)
+  // beat cooperative shuffle loads (680 / 679) and byte stores (~400-570).
+  const bool row_out = !ALIGNED && (reinterpret_cast<std::uintptr_t>(a.out) & 3) != 0;  // warp-uniform
   Block4 nxt[NB];
-  if (tile < full_tiles) {
+  auto load_tile = [&](unsigned long long t) {
 #pragma unroll
-    for (int j = 0; j < NB; ++j) nxt[j] = load_block<ALIGNED>(a.in + 16ull * (tile * kTile + lane + 32ull * j));
-  }
+    for (int j = 0; j < NB; ++j) nxt[j] = load_block<ALIGNED>(a.in + 16ull * (t * kTile + lane + 32ull * j));
+  };
+  if (tile < full_tiles) load_tile(tile);
   stage_tables<DEC>(sm);
   __syncthreads();
   const char* smb = reinterpret_cast<const char*>(sm);
@@ -271,13 +313,15 @@ __global__ void __launch_bounds__(kThreads, 1) ecb_kernel(const __grid_constant_
 #pragma unroll
     for (int j = 0; j < NB; ++j) s[j] = nxt[j];
     const unsigned long long next = tile + tstride;
-    if (next < full_tiles) {
-#pragma unroll
-      for (int j = 0; j < NB; ++j) nxt[j] = load_block<ALIGNED>(a.in + 16ull * (next * kTile + lane + 32ull * j));
-    }
+    if (next < full_tiles) load_tile(next);
     cipher<DEC, NB>(s, a.k.w, smb, lane4);
+    if (row_out) {
 #pragma unroll
-    for (int j = 0; j < NB; ++j) store_block<ALIGNED>(a.out + 16ull * (b0 + 32ull * j), s[j]);
+      for (int j = 0; j < NB; ++j) store_row_unaligned(a.out + 16ull * (b0 - lane + 32ull * j), s[j], lane);
+    } else {
+#pragma unroll
+      for (int j = 0; j < NB; ++j) store_block<ALIGNED>(a.out + 16ull * (b0 + 32ull * j), s[j]);
+    }
   }
   // the (at most one) ragged tile: partial blocks, pad block, trailer check
   for (; tile < ntiles; tile += tstride) {

@@ -104,3 +104,38 @@ def test_fuzz_batches(paes, gpu, orc):
             got = [h[o:o + L].tobytes() for o, L in zip(out_off, ol)]
             plan.close()
         assert got == want, case
+
+
+def test_unaligned_offsets_all_residues(paes, gpu, orc):
+    """Every byte offset 1..15 (funnel-shift loads; cooperative row stores for
+    non-word-aligned outputs), in place and with different input/output
+    offsets, at sizes that cross warp tiles and rows; the bytes around the
+    output must stay untouched."""
+    import torch
+
+    rnd = random.Random(1515)
+    key = rnd.randbytes(16)
+    rk = paes.round_keys(key)
+    for n in (16, 16 * 33, 16 * 64 + 7, 16 * 64 * 5 + 16 * 17 + 9, 3 << 20):
+        data = rnd.randbytes(n)
+        want = orc.encrypt_chunk(data, True, key)
+        m = len(want)
+        for off_in in range(16):
+            off_out = (off_in * 7 + 3) % 16 if off_in % 2 else off_in  # mixed and equal offsets
+            guard = 0xA5
+            src = torch.full((n + 64,), guard, dtype=torch.uint8, device="cuda")
+            src[off_in:off_in + n] = torch.frombuffer(bytearray(data), dtype=torch.uint8).cuda()
+            dst = torch.full((m + 64,), guard, dtype=torch.uint8, device="cuda")
+            assert paes.chunk_device(0, src.data_ptr() + off_in, n, True, rk, dst.data_ptr() + off_out) == m
+            h = dst.cpu().numpy()
+            assert h[off_out:off_out + m].tobytes() == want, (n, off_in, off_out)
+            assert (h[:off_out] == guard).all() and (h[off_out + m:] == guard).all(), (n, off_in, off_out)
+            # in place at the same offset, and back
+            buf = torch.full((m + 64,), guard, dtype=torch.uint8, device="cuda")
+            buf[off_in:off_in + n] = torch.frombuffer(bytearray(data), dtype=torch.uint8).cuda()
+            assert paes.chunk_device(0, buf.data_ptr() + off_in, n, True, rk, buf.data_ptr() + off_in) == m
+            assert buf[off_in:off_in + m].cpu().numpy().tobytes() == want, (n, off_in)
+            assert paes.chunk_device(1, buf.data_ptr() + off_in, m, True, rk, buf.data_ptr() + off_in) == n
+            hb = buf.cpu().numpy()
+            assert hb[off_in:off_in + n].tobytes() == data, (n, off_in)
+            assert (hb[:off_in] == guard).all() and (hb[off_in + m:] == guard).all(), (n, off_in)
