@@ -372,14 +372,14 @@ def decrypt_tensor(x, key: bytes, is_final: bool = True, out=None):
 
 def ecb_device(direction: int, d_in: int, d_out: int, nbytes: int, rk: bytes, device: int = 0, stream: int = 0):
     """Device-resident ECB on raw pointers (asynchronous on `stream`)."""
-    _raise(N.load().paes_cuda_ecb_device(direction, d_in, d_out, nbytes, rk, device, stream or None))
+    _raise(N.load().paes_cuda_ecb_device(direction, d_in, d_out, nbytes, _rk176(rk), device, stream or None))
 
 
 def chunk_device(direction: int, d_in: int, nbytes: int, is_final: bool, rk: bytes, d_out: int, device: int = 0,
                  stream: int = 0) -> int:
     olen = C.c_uint64()
-    _raise(N.load().paes_cuda_chunk_device(direction, d_in, nbytes, int(bool(is_final)), rk, d_out, C.byref(olen),
-                                           device, stream or None))
+    _raise(N.load().paes_cuda_chunk_device(direction, d_in, nbytes, int(bool(is_final)), _rk176(rk), d_out,
+                                           C.byref(olen), device, stream or None))
     return olen.value
 
 
@@ -390,13 +390,32 @@ def _u64_array(xs):
     return a, a.ctypes.data_as(C.POINTER(C.c_uint64))
 
 
+def _rk176(rk) -> bytes:
+    """An expanded schedule crosses the ABI as a bare pointer: check its size here."""
+    rk = bytes(rk)
+    if len(rk) != 176:
+        raise ValueError("round keys must be the 176-byte expanded schedule (round_keys(key))")
+    return rk
+
+
+def _batch_arrays(in_off, out_off, lens, rks):
+    """Descriptor arrays and per-message schedules for the batch calls; the C
+    ABI takes bare pointers, so the counts are checked here."""
+    n = len(lens)
+    if len(in_off) != n or len(out_off) != n:
+        raise ValueError("in_off, out_off and lens must have the same length")
+    rks = bytes(rks)
+    if len(rks) != 176 * n:
+        raise ValueError(f"rks must hold 176 bytes per message ({176 * n}), got {len(rks)}")
+    return n, [_u64_array(in_off), _u64_array(out_off), _u64_array(lens)], rks
+
+
 def ecb_batch(direction: int, d_in: int, d_out: int, in_off, out_off, lens, rks: bytes, pad: bool, device: int = 0,
               stream: int = 0):
     """One fused launch over n messages with per-message keys (config 5)."""
     import numpy as np
 
-    n = len(lens)
-    keep = [_u64_array(in_off), _u64_array(out_off), _u64_array(lens)]
+    n, keep, rks = _batch_arrays(in_off, out_off, lens, rks)
     olens = np.zeros(max(n, 1), dtype=np.uint64)
     _raise(N.load().paes_cuda_ecb_batch(direction, d_in, d_out, keep[0][1], keep[1][1], keep[2][1], rks, n,
                                         int(bool(pad)), olens.ctypes.data_as(C.POINTER(C.c_uint64)), device,
@@ -410,8 +429,7 @@ def ecb_batch_host(direction: int, h_in: int, h_out: int, in_off, out_off, lens,
     fused launch / D2H.  h_in / h_out are host addresses (pinned for speed)."""
     import numpy as np
 
-    n = len(lens)
-    keep = [_u64_array(in_off), _u64_array(out_off), _u64_array(lens)]
+    n, keep, rks = _batch_arrays(in_off, out_off, lens, rks)
     olens = np.zeros(max(n, 1), dtype=np.uint64)
     _raise(N.load().paes_cuda_batch_host(direction, h_in, h_out, keep[0][1], keep[1][1], keep[2][1], rks, n,
                                          int(bool(pad)), olens.ctypes.data_as(C.POINTER(C.c_uint64)), device))
@@ -423,11 +441,9 @@ class BatchPlan:
     on the device; run() is a single launch."""
 
     def __init__(self, direction: int, in_off, out_off, lens, rks: bytes, pad: bool, device: int = 0):
-        import numpy as np
-
-        self.n = len(lens)
+        self._h = None
+        self.n, (a, b, c), rks = _batch_arrays(in_off, out_off, lens, rks)
         h = C.c_void_p()
-        a, b, c = _u64_array(in_off), _u64_array(out_off), _u64_array(lens)
         _raise(N.load().paes_cuda_batch_plan_create(direction, a[1], b[1], c[1], rks, self.n, int(bool(pad)), device,
                                                     C.byref(h)))
         self._h = h

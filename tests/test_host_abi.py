@@ -238,3 +238,18 @@ def test_state_transform_errors_before_device(paes):
     with pytest.raises(ValueError):
         paes.state_transform(paes.ADD_ROUND_KEY, bytes(16))  # no round key
     assert paes.state_transform(paes.MIX_COLUMNS, b"") == b""
+
+
+def test_python_wrappers_check_what_the_abi_cannot(paes):
+    """Bare pointers cross the ABI, so the Python layer checks sizes first."""
+    rk = paes.round_keys(bytes(16))
+    with pytest.raises(ValueError, match="176 bytes per message"):
+        paes.ecb_batch(0, 1, 1, [0, 16], [0, 32], [16, 16], rk, True)  # one schedule for two messages
+    with pytest.raises(ValueError, match="same length"):
+        paes.ecb_batch_host(0, 1, 1, [0], [0, 16], [16], rk, True)
+    with pytest.raises(ValueError, match="176 bytes per message"):
+        paes.BatchPlan(0, [0], [0], [16], rk[:100], True)
+    with pytest.raises(ValueError, match="176-byte"):
+        paes.ecb_device(0, 1, 1, 16, bytes(16))
+    with pytest.raises(ValueError, match="176-byte"):
+        paes.chunk_device(0, 1, 16, True, rk + b"x", 1)
