@@ -158,7 +158,9 @@ int paes_cuda_chunk_device(int dir, const void* d_in, uint64_t len, int is_final
  * length of message i to out_lens[i] (host array) and returning PAES_EBADMSG
  * if any trailer is malformed (out_lens[i] = UINT64_MAX for those).  The
  * offset/length/key arrays are host memory; one fused kernel launch per call.
- * Synchronous when pad=1 and dir=DECRYPT, otherwise asynchronous on `stream`. */
+ * Offsets may be any byte offsets (messages at 16-byte-aligned addresses use
+ * the faster aligned kernel).  Synchronous when pad=1 and dir=DECRYPT,
+ * otherwise asynchronous on `stream`. */
 int paes_cuda_ecb_batch(int dir, const void* d_in, void* d_out, const uint64_t* in_off, const uint64_t* out_off,
                         const uint64_t* lens, const uint8_t* rks, uint32_t n, int pad, uint64_t* out_lens,
                         int device, void* stream);

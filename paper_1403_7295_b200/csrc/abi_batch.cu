@@ -23,6 +23,7 @@ namespace {
 // message (exec.cpp:375-392).
 struct BatchImage {
   bool dec = false, check = false;
+  bool aligned = true;  // every in/out offset a multiple of 16
   std::uint32_t n = 0;
   unsigned long long total_tiles = 0;  // warp tiles (each message owns whole tiles)
   std::size_t msg_bytes = 0, keys_off = 0, image_bytes = 0, status_off = 0, total_bytes = 0;
@@ -46,7 +47,7 @@ BatchImage plan_batch(int dir, const uint64_t* in_off, const uint64_t* out_off, 
   b.lens.assign(lens, lens + n);
   b.nblocks.resize(n);
   for (uint32_t i = 0; i < n; ++i) {
-    if (in_off[i] % 16 || out_off[i] % 16) throw std::invalid_argument("batch offsets must be multiples of 16");
+    if (in_off[i] % 16 || out_off[i] % 16) b.aligned = false;  // any byte offset works; aligned ones are faster
     if ((b.dec || !pad) && lens[i] % 16) throw std::invalid_argument("message length must be a multiple of 16");
     if (b.check && lens[i] == 0) throw PaddingError("unpad: length must be a non-zero multiple of 16");
     const unsigned long long nb = lens[i] / 16 + ((pad && !b.dec) ? 1 : 0);
@@ -88,6 +89,7 @@ BatchArgs batch_args(const BatchImage& b, const void* d_in, void* d_out, std::ui
   a.total_tiles = b.total_tiles;
   a.nmsg = b.n;
   a.check_pad = b.check ? 1u : 0u;
+  a.aligned = b.aligned ? 1u : 0u;
   return a;
 }
 
@@ -391,7 +393,19 @@ int paes_cuda_batch_host(int dir, const uint8_t* h_in, uint8_t* h_out, const uin
       }
       if (g.in_hi > g.in_lo) PAES_CK(copy_h2d_aligned(din, h_in + g.in_lo, g.in_hi - g.in_lo, s));
       PAES_CK(launch_batch(b.dec, batch_args(b, din, dout, dd), d.sm_count, s));
-      PAES_CK(copy_d2h_aligned(h_out + g.out_lo, dout, g.out_hi - g.out_lo, s));
+      // copy back only the messages' output bytes, merged where they touch:
+      // gaps between messages in h_out belong to the caller and are never
+      // written (a packed layout such as config 5 is still one copy per group)
+      std::vector<std::pair<std::uint64_t, std::uint64_t>> rs;
+      rs.reserve(g.count);
+      for (std::uint32_t i = g.first; i < g.first + g.count; ++i)
+        if (all.nblocks[i]) rs.emplace_back(out_off[i], out_off[i] + 16ull * all.nblocks[i]);
+      std::sort(rs.begin(), rs.end());
+      for (std::size_t r = 0; r < rs.size();) {
+        std::uint64_t lo = rs[r].first, hi = rs[r].second;
+        for (++r; r < rs.size() && rs[r].first <= hi; ++r) hi = std::max(hi, rs[r].second);
+        PAES_CK(copy_d2h_aligned(h_out + lo, dout + (lo - g.out_lo), hi - lo, s));
+      }
       if (b.check)
         PAES_CK(cudaMemcpyAsync(host + img_off[k] + b.status_off, dd + b.status_off, 4ull * b.n,
                                 cudaMemcpyDeviceToHost, s));

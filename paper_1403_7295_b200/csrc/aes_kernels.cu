@@ -351,7 +351,7 @@ __global__ void __launch_bounds__(kThreads, 1) ecb_kernel(const __grid_constant_
 // whole tiles (BatchMsg::first_tile), so a tile never mixes keys: a warp
 // reloads its 44 key registers only when it moves to the next message, and
 // the only per-block checks are on the message's ragged last tile.
-template <bool DEC, int NB>
+template <bool DEC, int NB, bool ALIGNED>
 __global__ void __launch_bounds__(kThreads, 1) batch_kernel(const __grid_constant__ BatchArgs a) {
   extern __shared__ __align__(16) std::uint32_t sm[];
   stage_tables<DEC>(sm);
@@ -423,25 +423,25 @@ __global__ void __launch_bounds__(kThreads, 1) batch_kernel(const __grid_constan
         for (int j = 0; j < NB; ++j) s[j] = nxt[j];
       } else {
 #pragma unroll
-        for (int j = 0; j < NB; ++j) s[j] = load_block<true>(src + 16ull * (lb + 32ull * j));
+        for (int j = 0; j < NB; ++j) s[j] = load_block<ALIGNED>(src + 16ull * (lb + 32ull * j));
       }
       if constexpr (kPrefetch) {
         have_nxt = tile + 1 < t_end && tile + 1 < next_first && t0 + 2 * kTile + a.check_pad <= msg.nfull;
         if (have_nxt) {
 #pragma unroll
-          for (int j = 0; j < NB; ++j) nxt[j] = load_block<true>(src + 16ull * (lb + kTile + 32ull * j));
+          for (int j = 0; j < NB; ++j) nxt[j] = load_block<ALIGNED>(src + 16ull * (lb + kTile + 32ull * j));
         }
       }
       cipher<DEC, NB>(s, kw, smb, lane4);
 #pragma unroll
-      for (int j = 0; j < NB; ++j) store_block<true>(dst + 16ull * (lb + 32ull * j), s[j]);
+      for (int j = 0; j < NB; ++j) store_block<ALIGNED>(dst + 16ull * (lb + 32ull * j), s[j]);
     } else {
       // the message's last tile: partial blocks, pad block, trailer check
       have_nxt = false;
 #pragma unroll
       for (int j = 0; j < NB; ++j) {
         const unsigned long long lb = t0 + lane + 32ull * j;
-        if (lb < msg.nfull) s[j] = load_block<true>(src + 16ull * lb);
+        if (lb < msg.nfull) s[j] = load_block<ALIGNED>(src + 16ull * lb);
         else if (lb < msg.nblocks) s[j] = pad_block(src + 16ull * msg.nfull, msg.tail_len);
         else s[j] = Block4{0, 0, 0, 0};
       }
@@ -450,7 +450,7 @@ __global__ void __launch_bounds__(kThreads, 1) batch_kernel(const __grid_constan
       for (int j = 0; j < NB; ++j) {
         const unsigned long long lb = t0 + lane + 32ull * j;
         if (lb < msg.nblocks) {
-          store_block<true>(dst + 16ull * lb, s[j]);
+          store_block<ALIGNED>(dst + 16ull * lb, s[j]);
           if (DEC && a.check_pad && lb == msg.nblocks - 1) a.status[m] = pad_check(s[j]);
         }
       }
@@ -576,8 +576,10 @@ cudaError_t prepare_kernels() {
   if ((e = set_smem(ecb_kernel<false, kNB, false>, kEncLaunchSmem))) return e;
   if ((e = set_smem(ecb_kernel<true, kNB, true>, kDecLaunchSmem))) return e;
   if ((e = set_smem(ecb_kernel<true, kNB, false>, kDecLaunchSmem))) return e;
-  if ((e = set_smem(batch_kernel<false, kNB>, kEncLaunchSmem))) return e;
-  if ((e = set_smem(batch_kernel<true, kNB>, kDecLaunchSmem))) return e;
+  if ((e = set_smem(batch_kernel<false, kNB, true>, kEncLaunchSmem))) return e;
+  if ((e = set_smem(batch_kernel<true, kNB, true>, kDecLaunchSmem))) return e;
+  if ((e = set_smem(batch_kernel<false, kNB, false>, kEncLaunchSmem))) return e;
+  if ((e = set_smem(batch_kernel<true, kNB, false>, kDecLaunchSmem))) return e;
   return cudaSuccess;
 }
 
@@ -607,8 +609,16 @@ cudaError_t launch_batch(bool dec, const BatchArgs& args, int sm_count, cudaStre
   const unsigned long long grid =
       args.total_tiles < static_cast<unsigned long long>(sm_count) ? args.total_tiles : sm_count;
   const int smem = dec ? kDecLaunchSmem : kEncLaunchSmem;
-  if (dec) batch_kernel<true, kNB><<<static_cast<unsigned>(grid), kThreads, smem, stream>>>(args);
-  else batch_kernel<false, kNB><<<static_cast<unsigned>(grid), kThreads, smem, stream>>>(args);
+  const bool aligned =
+      args.aligned && ((reinterpret_cast<std::uintptr_t>(args.in) | reinterpret_cast<std::uintptr_t>(args.out)) & 15) == 0;
+  const dim3 g(static_cast<unsigned>(grid));
+  if (dec) {
+    if (aligned) batch_kernel<true, kNB, true><<<g, kThreads, smem, stream>>>(args);
+    else batch_kernel<true, kNB, false><<<g, kThreads, smem, stream>>>(args);
+  } else {
+    if (aligned) batch_kernel<false, kNB, true><<<g, kThreads, smem, stream>>>(args);
+    else batch_kernel<false, kNB, false><<<g, kThreads, smem, stream>>>(args);
+  }
   g_launches.fetch_add(1, std::memory_order_relaxed);
   return cudaGetLastError();
 }

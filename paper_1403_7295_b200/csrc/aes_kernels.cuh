@@ -100,6 +100,7 @@ struct BatchArgs {
   unsigned long long total_tiles;
   std::uint32_t nmsg;
   std::uint32_t check_pad;
+  std::uint32_t aligned;  // host: every message start in and out is 16-byte aligned (picks the instantiation)
 };
 
 // Blocks per warp tile of the batch kernel (32 lanes x blocks per lane).

@@ -212,8 +212,6 @@ def test_missing_library_raises(tmp_path, monkeypatch):
 def test_batch_descriptor_errors_before_device(paes):
     """plan_batch validates every descriptor before touching a device."""
     rk = paes.round_keys(bytes(16))
-    with pytest.raises(ValueError, match="multiples of 16"):
-        paes.ecb_batch(0, 1, 1, [8], [0], [16], rk, True)
     with pytest.raises(ValueError, match="overflows"):
         paes.ecb_batch(0, 1, 1, [(1 << 64) - 16], [0], [32], rk, True)
     with pytest.raises(ValueError, match="overflows"):
