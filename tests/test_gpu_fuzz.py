@@ -42,7 +42,7 @@ def test_fuzz_host_and_device_paths(paes, gpu, orc):
                 src = torch.empty(n + 32, dtype=torch.uint8, pin_memory=True)
                 if n:
                     src[:n] = torch.frombuffer(bytearray(data), dtype=torch.uint8)
-                dst = torch.empty(n + 32, dtype=torch.uint8, pin_memory=True)
+                dst = torch.full((n + 32,), 0xC3, dtype=torch.uint8).pin_memory()
                 import ctypes as C
 
                 from paper_1403_7295_b200 import _native as N
@@ -51,6 +51,7 @@ def test_fuzz_host_and_device_paths(paes, gpu, orc):
                 rc = N.load().paes_cuda_chunk(0, src.data_ptr(), n, int(final), paes.round_keys(key), dst.data_ptr(),
                                               C.byref(olen), 1)
                 assert rc == 0 and dst[:olen.value].numpy().tobytes() == want_ct, (case, n, path)
+                assert (dst[olen.value:].numpy() == 0xC3).all(), (case, n, path)  # nothing written past out_len
             else:
                 off = rnd.choice([1, 3, 8]) if path == "device_unaligned" else 0
                 buf = torch.zeros(n + 64 + off, dtype=torch.uint8, device="cuda")
@@ -63,9 +64,11 @@ def test_fuzz_host_and_device_paths(paes, gpu, orc):
                     k = paes.chunk_device(1, buf.data_ptr(), m, final, rk, buf.data_ptr())
                     assert k == n and buf[:n].cpu().numpy().tobytes() == data, (case, n, path)
                 else:
-                    out = torch.zeros(n + 64 + off, dtype=torch.uint8, device="cuda")
+                    out = torch.full((n + 64 + off,), 0xC3, dtype=torch.uint8, device="cuda")
                     m = paes.chunk_device(0, buf.data_ptr() + off, n, final, rk, out.data_ptr() + off)
-                    assert out[off:off + m].cpu().numpy().tobytes() == want_ct, (case, n, path)
+                    h = out.cpu().numpy()
+                    assert h[off:off + m].tobytes() == want_ct, (case, n, path)
+                    assert (h[:off] == 0xC3).all() and (h[off + m:] == 0xC3).all(), (case, n, path)
     finally:
         paes.set_pipeline(64 << 20, 3)
 
