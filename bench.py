@@ -471,6 +471,9 @@ def run_b200(args, dist: Dist):
     if not args.no_e2e and n:
         e2e = run_e2e(args, dist, paes, torch, pt, n, out_n, is_final, rk, dev)
         e2e["numa"] = numa
+        # north_star: e2e also as a fraction of the kernel roofline (whole job,
+        # N x the per-GPU lookup-pipe bound); PCIe, not the kernel, bounds it
+        e2e["frac_of_kernel_roofline"] = round(e2e["value"] / (N * pipe_peak), 4)
 
     result = {
         "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": N, "steps": args.steps,
