@@ -356,11 +356,19 @@ int paes_cuda_batch_host(int dir, const uint8_t* h_in, uint8_t* h_out, const uin
     // small copy per group queued behind each input span cost ~8 % of the
     // PCIe rate, scripts/batch_host_probe.py).  Stream-ordered allocations
     // per group would let the pool serialise groups across streams.
-    if (d.obuf.empty()) {
-      for (int i = 0; i < S; ++i) {
-        std::uint8_t* p = nullptr;
-        PAES_CK(cudaMalloc(&p, C + 16));
-        d.obuf.push_back(p);
+    if (static_cast<int>(d.obuf.size()) != S) {  // all or nothing: a partial ring must not survive a failure
+      for (auto p : d.obuf) cudaFree(p);
+      d.obuf.clear();
+      try {
+        for (int i = 0; i < S; ++i) {
+          std::uint8_t* p = nullptr;
+          PAES_CK(cudaMalloc(&p, C + 16));
+          d.obuf.push_back(p);
+        }
+      } catch (...) {
+        for (auto p : d.obuf) cudaFree(p);
+        d.obuf.clear();
+        throw;
       }
     }
     if (d.dsc.empty()) {

@@ -163,6 +163,7 @@ cudaError_t launch_ecb_bitsliced_experiment(const std::uint8_t* in, std::uint8_t
   unsigned long long grid = (ntiles + kBsThreads / 32 - 1) / (kBsThreads / 32);
   const unsigned long long cap = static_cast<unsigned long long>(sm_count) * (per_sm > 0 ? per_sm : 1);
   if (grid > cap) grid = cap;
+  (void)cudaGetLastError();  // report this launch only
   ecb_bitsliced_kernel<<<static_cast<unsigned>(grid), kBsThreads, 0, stream>>>(in, out, ntiles, k);
   return cudaGetLastError();
 }

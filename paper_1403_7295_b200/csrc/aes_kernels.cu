@@ -583,11 +583,17 @@ cudaError_t prepare_kernels() {
   return cudaSuccess;
 }
 
+// Launchers report cudaGetLastError() after the launch; a stale non-sticky
+// error left by an earlier, unrelated call (ours or the caller's) is cleared
+// first, so the report covers this launch only.
+static void clear_stale_error() { (void)cudaGetLastError(); }
+
 cudaError_t launch_ecb(bool dec, const EcbArgs& args, int sm_count, cudaStream_t stream) {
   if (args.nblocks == 0) return cudaSuccess;
   // one CTA per SM, or one per warp tile when there are fewer tiles than SMs
   const unsigned long long ntiles = (args.nblocks + 32ull * kNB - 1) / (32ull * kNB);
   const unsigned long long grid = ntiles < static_cast<unsigned long long>(sm_count) ? ntiles : sm_count;
+  clear_stale_error();
   const bool aligned = ((reinterpret_cast<std::uintptr_t>(args.in) | reinterpret_cast<std::uintptr_t>(args.out)) & 15) == 0;
   const int smem = dec ? kDecLaunchSmem : kEncLaunchSmem;
   if (dec) {
@@ -609,6 +615,7 @@ cudaError_t launch_batch(bool dec, const BatchArgs& args, int sm_count, cudaStre
   const unsigned long long grid =
       args.total_tiles < static_cast<unsigned long long>(sm_count) ? args.total_tiles : sm_count;
   const int smem = dec ? kDecLaunchSmem : kEncLaunchSmem;
+  clear_stale_error();
   const bool aligned =
       args.aligned && ((reinterpret_cast<std::uintptr_t>(args.in) | reinterpret_cast<std::uintptr_t>(args.out)) & 15) == 0;
   const dim3 g(static_cast<unsigned>(grid));
@@ -626,6 +633,7 @@ cudaError_t launch_batch(bool dec, const BatchArgs& args, int sm_count, cudaStre
 cudaError_t launch_state_op(int op, std::uint8_t* d_states, unsigned long long n, const StateKey& rk,
                             cudaStream_t stream) {
   if (n == 0) return cudaSuccess;
+  clear_stale_error();
   state_op_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, stream>>>(op, d_states, n, rk);
   g_launches.fetch_add(1, std::memory_order_relaxed);
   return cudaGetLastError();
@@ -634,6 +642,7 @@ cudaError_t launch_state_op(int op, std::uint8_t* d_states, unsigned long long n
 cudaError_t launch_counter_fill(unsigned long long seed, unsigned long long word0, unsigned long long nwords, void* out,
                                 int sm_count, cudaStream_t stream) {
   if (nwords == 0) return cudaSuccess;
+  clear_stale_error();
   counter_fill_kernel<<<sm_count * 4, 512, 0, stream>>>(seed, word0, nwords, static_cast<unsigned long long*>(out));
   g_launches.fetch_add(1, std::memory_order_relaxed);
   return cudaGetLastError();
@@ -642,6 +651,7 @@ cudaError_t launch_counter_fill(unsigned long long seed, unsigned long long word
 cudaError_t launch_checksum(const void* buf, unsigned long long nwords, unsigned long long base, unsigned long long* d_out,
                             int sm_count, cudaStream_t stream) {
   if (nwords == 0) return cudaSuccess;
+  clear_stale_error();
   checksum_kernel<<<sm_count * 4, 512, 0, stream>>>(static_cast<const unsigned long long*>(buf), nwords, base, d_out);
   g_launches.fetch_add(1, std::memory_order_relaxed);
   return cudaGetLastError();
@@ -650,6 +660,7 @@ cudaError_t launch_checksum(const void* buf, unsigned long long nwords, unsigned
 cudaError_t launch_mismatch(const void* a, const void* b, unsigned long long nblocks, unsigned long long* d_out,
                             int sm_count, cudaStream_t stream) {
   if (nblocks == 0) return cudaSuccess;
+  clear_stale_error();
   mismatch_kernel<<<sm_count * 4, 512, 0, stream>>>(static_cast<const uint4*>(a), static_cast<const uint4*>(b), nblocks,
                                                    d_out);
   g_launches.fetch_add(1, std::memory_order_relaxed);

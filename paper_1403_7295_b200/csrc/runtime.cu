@@ -133,7 +133,8 @@ void ensure_pipeline(DevCtx& d, bool need_host) {
     chunk = g_chunk;
     ns = g_streams;
   }
-  if (d.chunk != chunk || static_cast<int>(d.st.size()) != ns) {
+  auto release = [&d] {
+    for (auto s : d.st) cudaStreamSynchronize(s);
     for (auto p : d.dbuf) cudaFree(p);
     for (auto p : d.hbuf) cudaFreeHost(p);
     for (auto p : d.obuf) cudaFree(p);
@@ -147,24 +148,44 @@ void ensure_pipeline(DevCtx& d, bool need_host) {
     d.dsc_cap.clear();
     d.st.clear();
     d.ev.clear();
-    d.chunk = chunk;
-    for (int i = 0; i < ns; ++i) {
-      cudaStream_t s;
-      PAES_CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
-      d.st.push_back(s);
-      cudaEvent_t e;
-      PAES_CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-      d.ev.push_back(e);
-      std::uint8_t* p = nullptr;
-      PAES_CK(cudaMalloc(&p, chunk + 16));
-      d.dbuf.push_back(p);
+    d.chunk = 0;  // unconfigured: the next call builds the ring afresh
+  };
+  // A failed allocation (e.g. a pipeline too large for the device) must not
+  // leave a half-built ring that later calls would index: everything is
+  // released and the context is marked unconfigured before the error leaves.
+  if (d.chunk != chunk || static_cast<int>(d.st.size()) != ns || static_cast<int>(d.dbuf.size()) != ns) {
+    release();
+    try {
+      for (int i = 0; i < ns; ++i) {
+        cudaStream_t s;
+        PAES_CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+        d.st.push_back(s);
+        cudaEvent_t e;
+        PAES_CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        d.ev.push_back(e);
+        std::uint8_t* p = nullptr;
+        PAES_CK(cudaMalloc(&p, chunk + 16));
+        d.dbuf.push_back(p);
+      }
+    } catch (...) {
+      release();
+      throw;
     }
+    d.chunk = chunk;
   }
-  if (need_host && d.hbuf.empty()) {
-    for (int i = 0; i < ns; ++i) {
-      std::uint8_t* p = nullptr;
-      PAES_CK(cudaMallocHost(&p, d.chunk + 16));
-      d.hbuf.push_back(p);
+  if (need_host && static_cast<int>(d.hbuf.size()) != ns) {
+    for (auto p : d.hbuf) cudaFreeHost(p);
+    d.hbuf.clear();
+    try {
+      for (int i = 0; i < ns; ++i) {
+        std::uint8_t* p = nullptr;
+        PAES_CK(cudaMallocHost(&p, d.chunk + 16));
+        d.hbuf.push_back(p);
+      }
+    } catch (...) {
+      for (auto p : d.hbuf) cudaFreeHost(p);
+      d.hbuf.clear();
+      throw;
     }
   }
 }

@@ -27,10 +27,17 @@ struct CudaFail {
   std::string msg;
 };
 
+// A failed call's error is also left in the runtime's per-thread "last
+// error" (non-sticky errors such as cudaErrorMemoryAllocation); it is
+// cleared here, so a later launch check (cudaGetLastError) does not report it
+// again after the caller has recovered.
 #define PAES_CK(call)                                                                           \
   do {                                                                                          \
     const cudaError_t e_ = (call);                                                              \
-    if (e_ != cudaSuccess) throw CudaFail{PAES_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e_)}; \
+    if (e_ != cudaSuccess) {                                                                    \
+      cudaGetLastError();                                                                       \
+      throw CudaFail{PAES_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e_)};            \
+    }                                                                                           \
   } while (0)
 
 // Runs `f`, mapping C++ exceptions to C-ABI codes (no exception crosses the ABI).

@@ -66,3 +66,25 @@ def test_ring_paths_vs_oracle(paes, gpu, orc, mode):
     finally:
         paes.set_pipeline(64 * MiB, 3)
         paes.set_zero_copy_max(128 * MiB)
+
+
+def test_oversized_pipeline_fails_cleanly_and_recovers(paes, gpu, orc):
+    """A staging ring too large for the device raises GpuError, leaves no
+    half-built ring behind, and the next call with a sane pipeline works."""
+    rnd = random.Random(77)
+    key = rnd.randbytes(16)
+    data = rnd.randbytes(3 * MiB + 5)  # pageable, > the 1 MiB bounce buffer: the staged ring
+    try:
+        paes.set_pipeline(16 << 30, 32)  # 32 x 16 GiB of device slots: cannot fit
+        with pytest.raises(paes.GpuError):
+            paes.encrypt_bytes(data, key)
+        with pytest.raises(paes.GpuError):  # same config again: still a clean failure, no stale ring
+            paes.encrypt_bytes(data, key)
+    finally:
+        paes.set_pipeline(64 * MiB, 3)
+    assert paes.encrypt_bytes(data, key) == orc.encrypt_chunk(data, True, key)
+    n = 2 * MiB
+    hin = np.frombuffer(rnd.randbytes(n), dtype=np.uint8).copy()
+    hout = np.zeros(n + 16, dtype=np.uint8)
+    ol = paes.ecb_batch_host(0, hin.ctypes.data, hout.ctypes.data, [0], [0], [n], paes.round_keys(key), True)
+    assert hout[: ol[0]].tobytes() == orc.encrypt_chunk(hin.tobytes(), True, key)
