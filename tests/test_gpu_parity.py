@@ -545,3 +545,35 @@ def test_no_writes_outside_outputs(paes, gpu, orc):
     for o, L in zip(out_off, olens):
         mask[o:o + L] = False
     assert (host[mask] == 0xA5).all()
+
+
+def test_multi_shard_pinned_zero_copy_and_ring(paes, gpu, orc):
+    """Pinned host buffers sharded over a 3-entry device list: every shard on
+    the zero-copy route, then (zero-copy off) on the copy ring."""
+    torch = _torch()
+    import ctypes as C
+
+    from paper_1403_7295_b200 import _native as N
+
+    L = N.load()
+    rnd = random.Random(3003)
+    key = rnd.randbytes(16)
+    rk = paes.round_keys(key)
+    paes.set_devices([0, 0, 0])
+    try:
+        for zc in (128 << 20, 0):
+            paes.set_zero_copy_max(zc)
+            for n in (16 * 3 + 5, 1 << 20, (9 << 20) + 3):
+                data = rnd.randbytes(n)
+                src = torch.empty(n + 32, dtype=torch.uint8, pin_memory=True)
+                src[:n] = torch.frombuffer(bytearray(data), dtype=torch.uint8)
+                dst = torch.zeros(n + 32, dtype=torch.uint8, pin_memory=True)
+                olen = C.c_uint64()
+                assert L.paes_cuda_chunk(0, src.data_ptr(), n, 1, rk, dst.data_ptr(), C.byref(olen), 3) == 0
+                assert dst[:olen.value].numpy().tobytes() == orc.encrypt_chunk(data, True, key), (zc, n)
+                back = C.c_uint64()
+                assert L.paes_cuda_chunk(1, dst.data_ptr(), olen.value, 1, rk, src.data_ptr(), C.byref(back), 3) == 0
+                assert back.value == n and src[:n].numpy().tobytes() == data, (zc, n)
+    finally:
+        paes.set_zero_copy_max(128 << 20)
+        paes.set_devices([])
