@@ -196,14 +196,14 @@ int paes_cuda_chunk_device(int dir, const void* d_in, uint64_t len, int is_final
       if (out_len) *out_len = a.nblocks * 16;
       return PAES_OK;
     }
-    std::lock_guard<std::mutex> lk(d.mu);
+    StatusSlot slot(d);  // a status word of this call's own: concurrent decrypts do not serialise
     EcbArgs a = make_args(r, static_cast<const std::uint8_t*>(d_in), static_cast<std::uint8_t*>(d_out), len, true,
-                          dec_key_words(rk), d.m_status);
+                          dec_key_words(rk), slot.dev());
     // the trailer check writes the mapped word itself: no memset / D2H copy
-    *reinterpret_cast<volatile std::uint32_t*>(d.h_status) = 0xffffffffu;  // sentinel: unchecked => PaddingError
+    *reinterpret_cast<volatile std::uint32_t*>(slot.host()) = 0xffffffffu;  // sentinel: unchecked => PaddingError
     PAES_CK(launch_ecb(true, a, d.sm_count, s));
     PAES_CK(cudaStreamSynchronize(s));
-    const std::uint32_t k = *reinterpret_cast<volatile std::uint32_t*>(d.h_status);
+    const std::uint32_t k = *reinterpret_cast<volatile std::uint32_t*>(slot.host());
     if (k == 0xffffffffu) throw PaddingError("unpad: invalid pad bytes");
     if (out_len) *out_len = len - k;
     return PAES_OK;

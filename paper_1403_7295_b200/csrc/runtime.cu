@@ -116,12 +116,36 @@ DevCtx& device(int id) {
     PAES_CK(prepare_kernels());
     PAES_CK(cudaHostAlloc(reinterpret_cast<void**>(&d.h_status), 4096, cudaHostAllocMapped | cudaHostAllocPortable));
     PAES_CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&d.m_status), d.h_status, 0));
+    {
+      std::lock_guard<std::mutex> sl(d.slot_mu);
+      d.free_slots.clear();
+      for (int i = 1024 - 1; i >= 1; --i) d.free_slots.push_back(i);  // 4096 B = 1024 words; word 0 is d.mu's
+    }
     PAES_CK(cudaMalloc(&d.d_acc, 64));
     PAES_CK(cudaMallocHost(&d.h_acc, 64));
     d.id = id;
     d.ready = true;
   }
   return d;
+}
+
+StatusSlot::StatusSlot(DevCtx& d) : d_(d) {
+  {
+    std::lock_guard<std::mutex> lk(d.slot_mu);
+    if (!d.free_slots.empty()) {
+      idx_ = d.free_slots.back();
+      d.free_slots.pop_back();
+      return;
+    }
+  }
+  fallback_ = std::unique_lock<std::mutex>(d.mu);  // all slots busy: word 0, serialised
+}
+
+StatusSlot::~StatusSlot() {
+  if (idx_ != 0) {
+    std::lock_guard<std::mutex> lk(d_.slot_mu);
+    d_.free_slots.push_back(idx_);
+  }
 }
 
 // Pipeline buffers (device rings + optional pinned host ring); d.mu held.

@@ -87,8 +87,10 @@ struct DevCtx {
   std::vector<std::size_t> dsc_cap;
   std::vector<cudaEvent_t> ev;
   std::uint64_t chunk = 0;
-  std::uint32_t* h_status = nullptr;  // pinned, mapped
+  std::uint32_t* h_status = nullptr;  // pinned, mapped; word 0 for host-pointer calls (d.mu held)
   std::uint32_t* m_status = nullptr;  // device alias of h_status: a one-shot check writes it directly
+  std::mutex slot_mu;                 // guards free_slots
+  std::vector<int> free_slots;        // status words 1.. for concurrent device-pointer final decrypts
   unsigned long long* d_acc = nullptr;
   unsigned long long* h_acc = nullptr;  // pinned
 };
@@ -98,6 +100,22 @@ constexpr int kMaxDev = 64;
 int visible_devices();
 // Lazily initialised context of device `id` (throws CudaFail ENODEV).
 DevCtx& device(int id);
+
+// A status word of its own for one device-pointer final decrypt, so
+// concurrent decrypts on different streams do not serialise on d.mu for the
+// length of their kernels.  Falls back to word 0 under d.mu if all are busy.
+class StatusSlot {
+ public:
+  explicit StatusSlot(DevCtx& d);
+  ~StatusSlot();
+  std::uint32_t* host() const { return d_.h_status + idx_; }
+  std::uint32_t* dev() const { return d_.m_status + idx_; }
+
+ private:
+  DevCtx& d_;
+  int idx_ = 0;
+  std::unique_lock<std::mutex> fallback_;
+};
 // Pipeline buffers (device ring, optional pinned host ring); d.mu held.
 void ensure_pipeline(DevCtx& d, bool need_host);
 // Pins the calling library-owned thread (and the threads it spawns) to the

@@ -99,3 +99,46 @@ def test_one_checked_plan_from_many_threads(paes, gpu, orc):
             assert all(ex.map(worker, range(4)))
     finally:
         plan.close()
+
+
+def test_concurrent_final_device_decrypts_keep_their_own_verdicts(paes, gpu, orc):
+    """Final device-pointer decrypts on private streams from many threads at
+    once, valid and wrong keys mixed: every call reads its own trailer status
+    (per-call status slots), never a neighbour's."""
+    import torch
+
+    rnd = random.Random(88)
+    jobs = []
+    for t in range(12):
+        key = rnd.randbytes(16)
+        data = rnd.randbytes(rnd.choice([16, 4096 + 3, 3 << 20]))
+        ct = orc.encrypt_chunk(data, True, key)
+        bad = t % 3 == 0
+        use_key = bytes([key[0] ^ 0x5A]) + key[1:] if bad else key
+        if bad:  # keep only wrong keys whose trailer is certainly invalid
+            try:
+                orc.decrypt_chunk(ct, True, use_key)
+                bad = False
+                use_key = key
+            except ValueError:
+                pass
+        jobs.append((data, ct, use_key, bad))
+
+    def run(job):
+        data, ct, key, bad = job
+        s = torch.cuda.Stream()
+        src = torch.frombuffer(bytearray(ct), dtype=torch.uint8).to("cuda")
+        dst = torch.zeros(len(ct), dtype=torch.uint8, device="cuda")
+        torch.cuda.synchronize()
+        ok = True
+        for _ in range(5):
+            try:
+                n = paes.chunk_device(1, src.data_ptr(), len(ct), True, paes.round_keys(key), dst.data_ptr(), 0,
+                                      s.cuda_stream)
+                ok &= (not bad) and n == len(data) and dst[:n].cpu().numpy().tobytes() == data
+            except paes.PaddingError:
+                ok &= bad
+        return ok
+
+    with ThreadPoolExecutor(12) as ex:
+        assert all(ex.map(run, jobs))
