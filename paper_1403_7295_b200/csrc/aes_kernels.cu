@@ -41,12 +41,13 @@ __device__ __forceinline__ void stage_tables(std::uint32_t* sm) {
   constexpr int kTabBytes = DEC ? kDecSmemBytes : kEncSmemBytes;
   constexpr int nvec = kTabBytes / 16;
   static_assert(nvec % kThreads == 0, "staging assumes whole passes");
-  static_assert(kThreads >= 256 + 64, "one scratch word per thread");
   // the CTA's single copy of the base table (+ InvS): 8-10 coalesced requests
   std::uint32_t* base = sm + kTabBytes / 4;
-  const int tid = static_cast<int>(threadIdx.x);
-  if (tid < 256) base[tid] = (DEC ? g_tab.td0 : g_tab.te0)[tid];
-  else if (DEC && tid < 256 + 64) base[tid] = reinterpret_cast<const std::uint32_t*>(g_tab.inv_sbox)[tid - 256];
+  constexpr int kScratchWords = 256 + (DEC ? 64 : 0);
+#pragma unroll
+  for (int w = static_cast<int>(threadIdx.x); w < kScratchWords; w += kThreads)
+    base[w] = w < 256 ? (DEC ? g_tab.td0 : g_tab.te0)[w]
+                      : reinterpret_cast<const std::uint32_t*>(g_tab.inv_sbox)[w - 256];
   __syncthreads();
   const std::uint8_t* inv_sbox = reinterpret_cast<const std::uint8_t*>(base + 256);
 #pragma unroll
