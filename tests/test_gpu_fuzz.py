@@ -1,12 +1,17 @@
 """Seeded differential fuzzing of every API path against the oracle: random
 lengths (weighted to block/tile/piece edges), directions, final flags,
 pointer offsets, aliasing and memory kinds; every output bit-exact."""
+import os
 import random
 
 import numpy as np
 import pytest
 
 pytestmark = pytest.mark.gpu
+# long campaigns: PAES_FUZZ_SCALE multiplies the case counts, PAES_FUZZ_SEED
+# shifts every seed (defaults: the suite's fixed, quick configuration)
+SCALE = max(1, int(os.environ.get("PAES_FUZZ_SCALE", "1")))
+SEED = int(os.environ.get("PAES_FUZZ_SEED", "0"))
 
 EDGES = [0, 1, 15, 16, 17, 31, 32, 33, 1023, 1024, 1025, 16 * 64 - 1, 16 * 64, 16 * 64 + 1, 65535, 65536, 65537,
          (1 << 20) - 1, 1 << 20, (1 << 20) + 1, (1 << 20) + 16 * 1024 + 3]
@@ -21,10 +26,10 @@ def rand_len(rnd):
 def test_fuzz_host_and_device_paths(paes, gpu, orc):
     import torch
 
-    rnd = random.Random(2026)
+    rnd = random.Random(2026 + SEED)
     paes.set_pipeline(256 * 1024, 3)  # small pieces so ~MiB inputs cross many piece boundaries
     try:
-        for case in range(160):
+        for case in range(160 * SCALE):
             n = rand_len(rnd)
             key = rnd.randbytes(16)
             data = rnd.randbytes(n)
@@ -76,8 +81,8 @@ def test_fuzz_host_and_device_paths(paes, gpu, orc):
 def test_fuzz_batches(paes, gpu, orc):
     import torch
 
-    rnd = random.Random(77)
-    for case in range(12):
+    rnd = random.Random(77 + SEED)
+    for case in range(12 * SCALE):
         nmsg = rnd.randrange(1, 90)
         lens = [rand_len(rnd) % (300 * 1024) for _ in range(nmsg)]
         keys = [rnd.randbytes(16) for _ in range(nmsg)]
@@ -116,7 +121,7 @@ def test_unaligned_offsets_all_residues(paes, gpu, orc):
     output must stay untouched."""
     import torch
 
-    rnd = random.Random(1515)
+    rnd = random.Random(1515 + SEED)
     key = rnd.randbytes(16)
     rk = paes.round_keys(key)
     for n in (16, 16 * 33, 16 * 64 + 7, 16 * 64 * 5 + 16 * 17 + 9, 3 << 20):
@@ -149,8 +154,8 @@ def test_batches_at_arbitrary_byte_offsets(paes, gpu, orc):
     batch API, both directions, trailer checks and untouched gaps."""
     import torch
 
-    rnd = random.Random(4242)
-    for case in range(6):
+    rnd = random.Random(4242 + SEED)
+    for case in range(6 * SCALE):
         nmsg = rnd.randrange(1, 60)
         lens = [rnd.choice([0, 1, 15, 16, 17, 1023, 4096 + 5, rnd.randrange(0, 200_000)]) for _ in range(nmsg)]
         keys = [rnd.randbytes(16) for _ in range(nmsg)]
