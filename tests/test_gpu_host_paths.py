@@ -88,3 +88,34 @@ def test_oversized_pipeline_fails_cleanly_and_recovers(paes, gpu, orc):
     hout = np.zeros(n + 16, dtype=np.uint8)
     ol = paes.ecb_batch_host(0, hin.ctypes.data, hout.ctypes.data, [0], [0], [n], paes.round_keys(key), True)
     assert hout[: ol[0]].tobytes() == orc.encrypt_chunk(hin.tobytes(), True, key)
+
+
+def test_batch_host_messages_larger_than_the_staging_chunk(paes, gpu, orc):
+    """A message longer than the pipeline chunk gets its own stream-ordered
+    device spans (batch_host's `fits == false` branch); neighbours stay in
+    normal groups."""
+    rnd = random.Random(5151)
+    paes.set_pipeline(1 * MiB, 3)
+    try:
+        lens = [100, 3 * MiB + 5, 7, 2 * MiB, 4096]
+        keys = [rnd.randbytes(16) for _ in lens]
+        msgs = [rnd.randbytes(L) for L in lens]
+        in_off, out_off, oi, oo = [], [], 0, 0
+        for L in lens:
+            in_off.append(oi)
+            out_off.append(oo)
+            oi += L + 3
+            oo += (L // 16 + 1) * 16 + 5
+        hin = np.zeros(oi, dtype=np.uint8)
+        for o, m in zip(in_off, msgs):
+            hin[o:o + len(m)] = np.frombuffer(m, dtype=np.uint8)
+        hout = np.full(oo, 0x77, dtype=np.uint8)
+        rks = b"".join(paes.round_keys(k) for k in keys)
+        ol = paes.ecb_batch_host(0, hin.ctypes.data, hout.ctypes.data, in_off, out_off, lens, rks, True)
+        for o, n, m, k in zip(out_off, ol, msgs, keys):
+            assert hout[o:o + n].tobytes() == orc.encrypt_chunk(m, True, k)
+        back = np.zeros(oo, dtype=np.uint8)
+        dl = paes.ecb_batch_host(1, hout.ctypes.data, back.ctypes.data, out_off, out_off, ol, rks, True)
+        assert [back[o:o + n].tobytes() for o, n in zip(out_off, dl)] == msgs
+    finally:
+        paes.set_pipeline(64 * MiB, 3)
