@@ -85,7 +85,9 @@ _lock = threading.Lock()
 
 
 def lib_path() -> str:
-    return _build.LIB
+    """The in-tree library, or a variant build named by PAES_CUDA_LIB (sanitizer,
+    coverage or tuning builds; there is still no fallback if it is missing)."""
+    return os.environ.get("PAES_CUDA_LIB") or _build.LIB
 
 
 def load(build_if_missing: bool = False):

@@ -14,6 +14,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -50,8 +51,11 @@ struct Map {
 // refuses mmap).  Its pages are allocated by the writer threads' own faults,
 // in parallel: preallocating with fallocate on a side thread was measured
 // slower (scripts/ab_file_variants.py, profiles/r01_file_prealloc_ab.json).
+// PAES_FILE_NO_MMAP=1 forces the pwrite path (file systems without shared
+// mmap take it on their own; the variable lets tests exercise it on tmpfs).
 void open_output(int fd, std::uint64_t cap, Map& map) {
   if (!cap || ::ftruncate(fd, static_cast<off_t>(cap)) != 0) return;
+  if (const char* v = std::getenv("PAES_FILE_NO_MMAP"); v && v[0] == '1') return;
   void* p = ::mmap(nullptr, cap, PROT_READ | PROT_WRITE, MAP_SHARED, fd, 0);
   if (p != MAP_FAILED) {
     map.p = static_cast<std::uint8_t*>(p);

@@ -81,3 +81,31 @@ def test_acceptance_roundtrip_200_files(paes, gpu, ref, eight_workers, tmp_path)
         assert back.read_bytes() == data, (i, size)
         rc, _, _, _ = ref.run_job(str(enc), str(back), key, w, 1, 1)
         assert rc == 0 and back.read_bytes() == data, (i, size)
+
+
+@pytest.mark.parametrize("no_mmap", ["0", "1"])
+def test_large_file_parallel_io_and_pwrite_path(paes, gpu, ref, eight_workers, tmp_path, monkeypatch, no_mmap):
+    """A file large enough that pread / write-back split across I/O threads
+    (pieces > 4 MiB), through the shared-mapping writer and (PAES_FILE_NO_MMAP=1)
+    the pwrite fallback; byte-identical to the reference's run_job."""
+    monkeypatch.setenv("PAES_FILE_NO_MMAP", no_mmap)
+    rnd = random.Random(909)
+    key = rnd.randbytes(16)
+    src = tmp_path / "big.bin"
+    data = rnd.randbytes((24 << 20) + 11)
+    src.write_bytes(data)
+    rc, _, _, _ = ref.run_job(str(src), str(tmp_path / "ref.enc"), key, 1, 0, 0)
+    assert rc == 0
+    for workers in (1, 2):
+        paes.encrypt_file(str(src), str(tmp_path / "gpu.enc"), key, workers=workers)
+        assert (tmp_path / "gpu.enc").read_bytes() == (tmp_path / "ref.enc").read_bytes(), workers
+        paes.decrypt_file(str(tmp_path / "gpu.enc"), str(tmp_path / "back.bin"), key, workers=workers)
+        assert (tmp_path / "back.bin").read_bytes() == data, workers
+
+
+def test_unknown_device_is_enodev(paes, gpu):
+    from paper_1403_7295_b200 import _native as N
+
+    with pytest.raises(paes.GpuError, match="no such CUDA device"):
+        paes.ecb_device(0, 1, 1, 16, paes.round_keys(bytes(16)), device=99)
+    assert N.load().paes_cuda_set_devices((N.C.c_int * 1)(99), 1) == N.ENODEV
