@@ -80,7 +80,7 @@ int paes_cuda_device_count(void);
 int paes_cuda_set_devices(const int* ids, int n);
 /* Host-pointer pipeline tuning: staging chunk (bytes, a multiple of 16 and
  * >= 4096) and streams per device (1..32).  0 keeps the current value.
- * Defaults 64 MiB, 3. */
+ * Defaults 256 MiB, 3. */
 int paes_cuda_set_pipeline(uint64_t chunk_bytes, int streams);
 /* Pinned host ranges up to this many bytes (per device shard) skip the copy
  * ring: one kernel reads and writes the caller's pinned buffers over PCIe

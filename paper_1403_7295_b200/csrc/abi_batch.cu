@@ -304,8 +304,12 @@ int paes_cuda_batch_host(int dir, const uint8_t* h_in, uint8_t* h_out, const uin
     std::lock_guard<std::mutex> lk(d.mu);
     ensure_pipeline(d, false);
     QuiesceOnThrow quiesce{d};
-    const std::uint64_t C = d.chunk;
+    const std::uint64_t cap = d.chunk;  // ring slot capacity
     const int S = static_cast<int>(d.st.size());
+    // group target: the ring's piece-size model over the batch's input bytes
+    std::uint64_t in_bytes = 0;
+    for (std::uint32_t i = 0; i < n; ++i) in_bytes += lens[i];
+    const std::uint64_t C = piece_size(in_bytes, cap, S);
     // groups of consecutive messages whose input and output spans stay <= C
     struct Group {
       std::uint32_t first, count;
@@ -362,7 +366,7 @@ int paes_cuda_batch_host(int dir, const uint8_t* h_in, uint8_t* h_out, const uin
       try {
         for (int i = 0; i < S; ++i) {
           std::uint8_t* p = nullptr;
-          PAES_CK(cudaMalloc(&p, C + 16));
+          PAES_CK(cudaMalloc(&p, cap + 16));
           d.obuf.push_back(p);
         }
       } catch (...) {
@@ -391,7 +395,7 @@ int paes_cuda_batch_host(int dir, const uint8_t* h_in, uint8_t* h_out, const uin
       const Group& g = groups[k];
       const BatchImage& b = imgs[k];
       cudaStream_t s = d.st[k % S];
-      const bool fits = g.in_hi - g.in_lo <= C + 16 && g.out_hi - g.out_lo <= C + 16;
+      const bool fits = g.in_hi - g.in_lo <= cap + 16 && g.out_hi - g.out_lo <= cap + 16;
       std::uint8_t* din = d.dbuf[k % S];
       std::uint8_t* dout = d.obuf[k % S];
       std::uint8_t* dd = dimg + img_off[k];

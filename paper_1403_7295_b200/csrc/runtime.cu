@@ -18,6 +18,7 @@
 
 #include <algorithm>
 #include <cctype>
+#include <cmath>
 #include <cerrno>
 #include <chrono>
 #include <cstdio>
@@ -43,7 +44,9 @@ int fail(int code, const std::string& msg) {
 DevCtx g_dev[kMaxDev];
 std::mutex g_cfg_mu;
 std::vector<int> g_devices;  // empty = all visible
-std::uint64_t g_chunk = 64ull << 20;  // scripts/pcie_probe.py: 64-128 MiB pieces reach ~94% of concurrent H2D+D2H
+// Ring shape: 3 streams, slots of 256 MiB (piece_size() uses the full slot
+// only for ranges beyond ~16 GiB; see there).
+std::uint64_t g_chunk = 256ull << 20;
 int g_streams = 3;
 std::atomic<std::uint64_t> g_zero_copy_max{128ull << 20};  // scripts/zero_copy_probe.cu
 
@@ -249,12 +252,21 @@ EcbArgs make_args(const Range& r, const std::uint8_t* in, std::uint8_t* out, std
   return a;
 }
 
-// Piece size for a range: the staging chunk, but small enough that even a
-// short range is split into ~2 pieces per stream so copy-in, kernel and
-// copy-out still overlap (a single 64 MiB piece would serialise them).
+// Piece size for a range, from measurements on the box (pinned and staged
+// paths, in and out of place; scripts/e2e_ring_sweep.py, pcie_probe.py,
+// pageable_probe.py):
+// - short ranges: ~2 pieces per stream so copy-in, kernel and copy-out overlap;
+// - up to ~16 GiB: 64 MiB pieces (1 GiB: 46.1 GB/s at 64 MiB against 44.6 at
+//   both 33 MB and 128 MiB; smaller pieces also cost the staged path its copy
+//   threads' spawn per piece);
+// - beyond: len / 256, up to the ring slot (64 GiB in place: 49.3 GB/s at
+//   256 MiB against 48.3 at 64 MiB -- fewer per-piece gaps).
 std::uint64_t piece_size(std::uint64_t len, std::uint64_t chunk, int streams) {
+  constexpr std::uint64_t kMid = 64ull << 20;
   const std::uint64_t floor_piece = std::min<std::uint64_t>(4ull << 20, chunk);
-  const std::uint64_t p = (len / (2ull * static_cast<std::uint64_t>(streams)) + 15) & ~std::uint64_t(15);
+  std::uint64_t p = len / (2ull * static_cast<std::uint64_t>(streams));
+  if (p > kMid) p = std::max(kMid, len / 256);
+  p = (p + 15) & ~std::uint64_t(15);
   return std::clamp(p, floor_piece, chunk);
 }
 

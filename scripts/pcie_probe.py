@@ -65,7 +65,7 @@ def e2e_grid(n=8 * GiB):
                 assert rc == 0, N.last_error()
             el = (time.perf_counter() - t) / 2
             out[f"{chunk}MiBx{streams}"] = round(n / el / 1e9, 2)
-    paes.set_pipeline(64 * MiB, 3)
+    paes.set_pipeline(256 * MiB, 3)  # the library default
     return out
 
 

@@ -148,7 +148,7 @@ int main(int argc, char** argv) {
   std::vector<std::thread> pool;
   for (int t = 0; t < threads; ++t) pool.emplace_back(worker, t, iters);
   for (auto& t : pool) t.join();
-  paes_cuda_set_pipeline(64ull << 20, 3);
+  paes_cuda_set_pipeline(256ull << 20, 3);
   std::printf("stress: %d threads x %d ops, %d failures\n", threads, iters, g_fail.load());
   return g_fail.load();
 }

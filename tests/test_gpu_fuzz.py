@@ -75,7 +75,7 @@ def test_fuzz_host_and_device_paths(paes, gpu, orc):
                     assert h[off:off + m].tobytes() == want_ct, (case, n, path)
                     assert (h[:off] == 0xC3).all() and (h[off + m:] == 0xC3).all(), (case, n, path)
     finally:
-        paes.set_pipeline(64 << 20, 3)
+        paes.set_pipeline(256 << 20, 3)
 
 
 def test_fuzz_batches(paes, gpu, orc):

@@ -64,7 +64,7 @@ def test_ring_paths_vs_oracle(paes, gpu, orc, mode):
                 k = _run(paes, 1, dp, m, True, bad, dp)
                 assert read(k) == expect
     finally:
-        paes.set_pipeline(64 * MiB, 3)
+        paes.set_pipeline(256 * MiB, 3)
         paes.set_zero_copy_max(128 * MiB)
 
 
@@ -81,7 +81,7 @@ def test_oversized_pipeline_fails_cleanly_and_recovers(paes, gpu, orc):
         with pytest.raises(paes.GpuError):  # same config again: still a clean failure, no stale ring
             paes.encrypt_bytes(data, key)
     finally:
-        paes.set_pipeline(64 * MiB, 3)
+        paes.set_pipeline(256 * MiB, 3)
     assert paes.encrypt_bytes(data, key) == orc.encrypt_chunk(data, True, key)
     n = 2 * MiB
     hin = np.frombuffer(rnd.randbytes(n), dtype=np.uint8).copy()
@@ -118,4 +118,4 @@ def test_batch_host_messages_larger_than_the_staging_chunk(paes, gpu, orc):
         dl = paes.ecb_batch_host(1, hout.ctypes.data, back.ctypes.data, out_off, out_off, ol, rks, True)
         assert [back[o:o + n].tobytes() for o, n in zip(out_off, dl)] == msgs
     finally:
-        paes.set_pipeline(64 * MiB, 3)
+        paes.set_pipeline(256 * MiB, 3)

@@ -127,7 +127,7 @@ def test_pipeline_piece_boundaries(paes, gpu, orc):
             assert ct == orc.encrypt_chunk(data, True, key), n
             assert paes.decrypt_bytes(ct, key) == data
     finally:
-        paes.set_pipeline(64 * MiB, 3)
+        paes.set_pipeline(256 * MiB, 3)
 
 
 def test_in_place_host(paes, gpu, orc):
@@ -247,7 +247,7 @@ def test_file_pipeline_many_pieces(paes, gpu, orc, tmp_path):
         paes.decrypt_file(str(tmp_path / "b"), str(tmp_path / "c"), key)
         assert (tmp_path / "c").read_bytes() == data
     finally:
-        paes.set_pipeline(64 * MiB, 3)
+        paes.set_pipeline(256 * MiB, 3)
 
 
 # ------------------------------------------------------------ BASELINE.json configs
@@ -501,7 +501,7 @@ def test_batch_host_pipeline(paes, gpu, orc):
         for i in range(n):
             assert back[out_off[i]:out_off[i] + lens[i]].tobytes() == hin[in_off[i]:in_off[i] + lens[i]].tobytes()
     finally:
-        paes.set_pipeline(64 * MiB, 3)
+        paes.set_pipeline(256 * MiB, 3)
 
 
 def test_no_writes_outside_outputs(paes, gpu, orc):
