@@ -4,8 +4,10 @@ Same names, argument meaning and error behaviour as
 proj/python/paes_module.cpp (see the per-function citations), so the
 reference's own smoke tests read the same against this engine; every compute
 call goes through the C ABI (include/paes_cuda.h) into the sm_100a kernels.
-The only strategy is ``"gpu"`` (the reference's "sequential"/"threads"/
-"processes" CPU strategies are what this engine replaces).
+Every compute path is the GPU engine: ``strategy="gpu"`` names it, and the
+reference's own "sequential"/"threads"/"processes" names are accepted too and
+run the same GPU pipeline (their outputs are identical by the reference's own
+tests), so callers need not change their arguments.
 
 Exceptions (paes_module.cpp:153-155): PaddingError -> ValueError,
 WorkerError -> RuntimeError, IoError -> OSError.  CUDA failures raise
@@ -292,14 +294,40 @@ def reject_outliers(samples: Iterable[float]) -> List[float]:
 
 
 # ---------------------------------------------------------------- files
+# The reference's CPU strategy names (strategy_from_string exec.cpp:33-38).
+# They all produce the same bytes (test_smoke.py:77-78; test_exec.cpp:64-86),
+# so a caller written against `_paes` keeps its strategy argument and runs on
+# the GPU pipeline: `workers` there counts CPU workers, so it is clamped to
+# the visible GPUs.  worker_exe only named the process strategy's worker
+# binary and is not needed.
+REFERENCE_STRATEGIES = ("sequential", "threads", "processes")
+
+
 def _job(direction: int, input: str, output: str, key: bytes, workers: int, strategy: str, worker_exe: str):
-    if strategy != "gpu":
-        raise ValueError("strategy must be gpu (this engine replaces the sequential/threads/processes CPU strategies)")
+    if strategy not in REFERENCE_STRATEGIES and strategy != "gpu":
+        # to_strategy paes_module.cpp:43-46
+        raise ValueError("strategy must be sequential, threads, processes or gpu")
     if workers < 0:
         raise ValueError("workers must be >= 0")
+    if strategy in ("threads", "processes") and workers == 0:
+        # run_threaded exec.cpp:209 / run_process_isolated exec.cpp:273
+        raise ValueError(f"run_{'threaded' if strategy == 'threads' else 'process_isolated'}: workers must be >= 1")
     key = _as_key(key)
+    if strategy == "sequential":
+        workers = 1  # run_sequential exec.cpp:206 ignores workers
+    elif strategy in REFERENCE_STRATEGIES:
+        workers = max(1, min(workers, device_count()))
     o = N.JobOutcome()
-    _raise(N.load().paes_cuda_run_job(os.fsencode(input), os.fsencode(output), key, workers, direction, C.byref(o)))
+    try:
+        _raise(N.load().paes_cuda_run_job(os.fsencode(input), os.fsencode(output), key, workers, direction,
+                                          C.byref(o)))
+    except WorkerError as e:
+        # run_sequential runs its one chunk inline, so a bad trailer surfaces
+        # as the PaddingError itself, not wrapped (exec.cpp:184-186 vs :206)
+        inner = str(e).split(": ", 2)[-1]
+        if strategy == "sequential" and inner.startswith("unpad:"):
+            raise PaddingError(inner) from None
+        raise
     return {"bytes_in": o.bytes_in, "bytes_out": o.bytes_out, "seconds": o.seconds}
 
 

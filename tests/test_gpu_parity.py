@@ -236,6 +236,48 @@ def test_file_roundtrip_and_failure(paes, gpu, orc, tmp_path):
         paes.decrypt_file(str(tmp_path / "e.bin"), str(tmp_path / "x.bin"), key)
 
 
+def test_reference_strategy_names_through_paes_alias(paes, gpu, orc, tmp_path):
+    """test_smoke.py:62-78 as a `_paes` caller writes it (strategy="threads",
+    workers 4 then 2), plus "sequential" and "processes": every name runs the
+    GPU pipeline and the bytes match the reference's in-memory path."""
+    import importlib
+    import sys
+
+    compat = os.path.join(os.path.dirname(paes.__file__), "compat")
+    sys.path.insert(0, compat)
+    try:
+        _paes = importlib.import_module("_paes")
+    finally:
+        sys.path.remove(compat)
+        sys.modules.pop("_paes", None)
+    key = bytes.fromhex("000102030405060708090a0b0c0d0e0f")
+    data = random.Random(62).randbytes(100_000)  # fixed: the wrong key below must give a bad trailer
+    src = tmp_path / "plain.bin"
+    src.write_bytes(data)
+    want = orc.encrypt_chunk(data, True, key)
+    enc = _paes.encrypt_file(str(src), str(tmp_path / "c.bin"), key, workers=4, strategy="threads")
+    assert enc["bytes_in"] == len(data) and enc["bytes_out"] == (len(data) // 16 + 1) * 16
+    dec = _paes.decrypt_file(str(tmp_path / "c.bin"), str(tmp_path / "p.bin"), key, workers=2, strategy="threads")
+    assert dec["bytes_out"] == len(data)
+    assert (tmp_path / "p.bin").read_bytes() == data
+    assert (tmp_path / "c.bin").read_bytes() == _paes.encrypt_bytes(data, key) == want
+    for strategy, workers in (("sequential", 8), ("processes", 3)):
+        out = tmp_path / f"c_{strategy}.bin"
+        _paes.encrypt_file(str(src), str(out), key, workers=workers, strategy=strategy, worker_exe="/unused")
+        assert out.read_bytes() == want
+    # default strategy, as the reference's default "sequential" call reads
+    _paes.encrypt_file(str(src), str(tmp_path / "c_default.bin"), key)
+    assert (tmp_path / "c_default.bin").read_bytes() == want
+    bad = bytes([key[0] ^ 1]) + key[1:]
+    with pytest.raises(ValueError):  # WorkerError is a RuntimeError; PaddingError a ValueError
+        _paes.decrypt_bytes(_paes.encrypt_bytes(b"hello world", key), bad)
+    with pytest.raises(RuntimeError, match=r"worker failure: chunk \d+: unpad"):
+        _paes.decrypt_file(str(tmp_path / "c.bin"), str(tmp_path / "bad.bin"), bad, workers=2, strategy="threads")
+    with pytest.raises(_paes.PaddingError, match="^unpad"):  # sequential: not wrapped (exec.cpp:206)
+        _paes.decrypt_file(str(tmp_path / "c.bin"), str(tmp_path / "bad.bin"), bad, strategy="sequential")
+    assert not (tmp_path / "bad.bin").exists()
+
+
 def test_file_pipeline_many_pieces(paes, gpu, orc, tmp_path):
     paes.set_pipeline(64 * 1024, 3)
     try:

@@ -186,8 +186,13 @@ def test_argument_errors_before_device(paes):
         paes.encrypt_chunk(bytes(17), False, bytes(16))
     with pytest.raises(paes.PaddingError):
         paes.decrypt_bytes(b"", bytes(16))
-    with pytest.raises(ValueError):
-        paes.encrypt_file("/nonexistent", "/tmp/x", bytes(16), strategy="threads")
+    with pytest.raises(ValueError, match="strategy must be"):
+        paes.encrypt_file("/nonexistent", "/tmp/x", bytes(16), strategy="fibers")
+    # the reference's worker-count rule for its parallel strategies (exec.cpp:209, 273)
+    with pytest.raises(ValueError, match="run_threaded: workers must be >= 1"):
+        paes.encrypt_file("/nonexistent", "/tmp/x", bytes(16), workers=0, strategy="threads")
+    with pytest.raises(ValueError, match="run_process_isolated: workers must be >= 1"):
+        paes.decrypt_file("/nonexistent", "/tmp/x", bytes(16), workers=0, strategy="processes")
     from paper_1403_7295_b200 import _native as N
 
     L = N.load()
@@ -198,6 +203,27 @@ def test_argument_errors_before_device(paes):
     assert L.paes_cuda_set_pipeline(0, 33) == N.EINVAL
     assert L.paes_cuda_set_pipeline(0, -1) == N.EINVAL
     assert L.paes_cuda_set_pipeline(0, 0) == 0  # 0 keeps the current values
+
+
+def test_paes_alias_module(paes):
+    """`import _paes` from the compat directory is this engine under the reference's module name."""
+    import importlib
+    import sys
+
+    compat = os.path.join(os.path.dirname(paes.__file__), "compat")
+    sys.path.insert(0, compat)
+    try:
+        sys.modules.pop("_paes", None)
+        alias = importlib.import_module("_paes")
+    finally:
+        sys.path.remove(compat)
+        sys.modules.pop("_paes", None)
+    for name in ("encrypt_block", "decrypt_block", "expand_key", "encrypt_bytes", "decrypt_bytes", "pkcs7_pad",
+                 "pkcs7_unpad", "plan_chunks", "reject_outliers", "encrypt_file", "decrypt_file", "csv_header",
+                 "PaddingError", "WorkerError", "IoError"):
+        assert getattr(alias, name) is getattr(paes, name), name
+    assert alias.expand_key(bytes(16))[1].hex() == "62636363" * 4  # test_aes.cpp:120-124
+    assert [c["raw_len"] for c in alias.plan_chunks(1000, 4)] == [256, 256, 256, 232]  # test_smoke.py:48-53
 
 
 def test_missing_library_raises(tmp_path, monkeypatch):
