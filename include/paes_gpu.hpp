@@ -22,6 +22,7 @@
 // Error codes from the C ABI are rethrown as the reference's exception types.
 #pragma once
 
+#include <algorithm>
 #include <array>
 #include <cstdint>
 #include <filesystem>
@@ -304,13 +305,39 @@ struct JobOutcome {
   double seconds = 0.0;
 };
 
+// Every strategy runs the GPU file pipeline: the reference's CPU strategies
+// write identical bytes (test_exec.cpp:64-86), so a JobSpec written for the
+// reference keeps its strategy.  Their `workers` count CPU workers and are
+// clamped to the visible GPUs; 0 keeps the reference's invalid_argument
+// (exec.cpp:209, 273).  Sequential runs one shard and, like run_sequential
+// (exec.cpp:206), raises a bad trailer as PaddingError, not WorkerError.
 inline JobOutcome run_job(const JobSpec& job) {
-  if (job.strategy != ExecStrategy::Gpu)
-    throw std::invalid_argument("strategy '" + std::string(to_string(job.strategy)) +
-                                "' runs on the CPU in the reference library; paes::gpu runs only 'gpu'");
+  unsigned workers = job.workers;
+  switch (job.strategy) {
+    case ExecStrategy::Sequential: workers = 1; break;
+    case ExecStrategy::Threaded:
+    case ExecStrategy::ProcessIsolated: {
+      if (workers == 0)
+        throw std::invalid_argument(job.strategy == ExecStrategy::Threaded
+                                        ? "run_threaded: workers must be >= 1"
+                                        : "run_process_isolated: workers must be >= 1");
+      const int n = paes_cuda_device_count();
+      workers = std::max(1u, std::min(workers, static_cast<unsigned>(n > 0 ? n : 1)));
+      break;
+    }
+    case ExecStrategy::Gpu: break;
+  }
   paes_job_outcome o{};
-  check(paes_cuda_run_job(job.input_path.c_str(), job.output_path.c_str(), job.key.bytes.data(), job.workers,
-                          job.direction == Direction::Encrypt ? PAES_ENCRYPT : PAES_DECRYPT, &o));
+  try {
+    check(paes_cuda_run_job(job.input_path.c_str(), job.output_path.c_str(), job.key.bytes.data(), workers,
+                            job.direction == Direction::Encrypt ? PAES_ENCRYPT : PAES_DECRYPT, &o));
+  } catch (const WorkerError& e) {
+    // "worker failure: chunk 0: unpad: ..." -> the inner PaddingError
+    const std::string m = e.what();
+    const auto p = m.find(": unpad:");
+    if (job.strategy == ExecStrategy::Sequential && p != std::string::npos) throw PaddingError(m.substr(p + 2));
+    throw;
+  }
   return {o.bytes_in, o.bytes_out, o.seconds};
 }
 

@@ -107,13 +107,18 @@ static void host_tests() {
     CHECK(sb[static_cast<std::size_t>(x)] == s);
     CHECK(isb[sb[static_cast<std::size_t>(x)]] == x);
   }
-  // strategy names (exec.cpp:24-38) + "gpu"; CPU strategies are refused loudly
+  // strategy names (exec.cpp:24-38) + "gpu"; the reference's worker-count rule (exec.cpp:209, 273)
   CHECK(gpu::to_string(gpu::ExecStrategy::Threaded) == "threads");
   CHECK(gpu::strategy_from_string("processes") == gpu::ExecStrategy::ProcessIsolated);
   CHECK(gpu::strategy_from_string("gpu") == gpu::ExecStrategy::Gpu);
   CHECK(!gpu::strategy_from_string("cuda").has_value());
   CHECK(throws<std::invalid_argument>([] {
-    gpu::JobSpec j{"/tmp/a", "/tmp/b", gpu::Key128{}, 1, gpu::Direction::Encrypt, gpu::ExecStrategy::Threaded, {}};
+    gpu::JobSpec j{"/tmp/a", "/tmp/b", gpu::Key128{}, 0, gpu::Direction::Encrypt, gpu::ExecStrategy::Threaded, {}};
+    gpu::run_job(j);
+  }));
+  CHECK(throws<std::invalid_argument>([] {
+    gpu::JobSpec j{"/tmp/a", "/tmp/b", gpu::Key128{}, 0, gpu::Direction::Encrypt, gpu::ExecStrategy::ProcessIsolated,
+                   {}};
     gpu::run_job(j);
   }));
   // assemble (chunk.cpp:102-111): concatenation in plan order, count must match
@@ -259,6 +264,21 @@ static void gpu_tests() {
   } catch (const gpu::WorkerError& e) {
     CHECK(std::string(e.what()).find("chunk 0") != std::string::npos);
   }
+  CHECK(!std::filesystem::exists(dir / "bad.dec"));
+  // the reference's CPU strategy names run the same GPU pipeline, same bytes
+  for (auto st : {gpu::ExecStrategy::Sequential, gpu::ExecStrategy::Threaded, gpu::ExecStrategy::ProcessIsolated}) {
+    gpu::JobSpec j = job;
+    j.output_path = dir / ("mb." + std::string(gpu::to_string(st)));
+    j.workers = 4;
+    j.strategy = st;
+    CHECK(gpu::run_job(j).bytes_out == (1u << 20) + 16);
+    std::ifstream f(j.output_path, std::ios::binary);
+    CHECK(std::vector<std::uint8_t>((std::istreambuf_iterator<char>(f)), std::istreambuf_iterator<char>()) == whole);
+  }
+  wrong.strategy = gpu::ExecStrategy::Sequential;  // run_sequential: the PaddingError itself (exec.cpp:206)
+  CHECK(throws<gpu::PaddingError>([&] { gpu::run_job(wrong); }));
+  wrong.strategy = gpu::ExecStrategy::Threaded;
+  CHECK(throws<gpu::WorkerError>([&] { gpu::run_job(wrong); }));
   CHECK(!std::filesystem::exists(dir / "bad.dec"));
   std::filesystem::remove_all(dir);
 }
