@@ -14,7 +14,7 @@
 //   encrypt_chunk / decrypt_chunk               gpu::encrypt_chunk / decrypt_chunk   (exec.hpp:61-65)
 //   plan_chunks / plan_decrypt_chunks           gpu::plan_chunks / ...               (chunk.hpp:37-47)
 //   pad_final / unpad_final                     gpu::pad_final / unpad_final         (chunk.hpp:49-54)
-//   run_job(JobSpec) + ExecStrategy             gpu::run_job (strategy "gpu")        (exec.hpp:18-51)
+//   run_job(JobSpec) + ExecStrategy             gpu::run_job (every strategy on GPU) (exec.hpp:18-51)
 //   run_worker_chunk(WorkerChunkArgs)           gpu::run_worker_chunk                (exec.hpp:46-59)
 //   assemble(plan, chunks)                      gpu::assemble                        (chunk.hpp:57-58)
 //   Error / IoError / PaddingError / WorkerError  same names, same bases           (errors.hpp:8-33)
