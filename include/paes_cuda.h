@@ -84,9 +84,11 @@ int paes_cuda_set_devices(const int* ids, int n);
 int paes_cuda_set_pipeline(uint64_t chunk_bytes, int streams);
 /* Pinned host ranges up to this many bytes (per device shard) skip the copy
  * ring: one kernel reads and writes the caller's pinned buffers over PCIe
- * through their UVA aliases.  0 disables.  Default 128 MiB
- * (profiles/r01_zero_copy_probe.json).  cudaHostRegister'ed buffers (default
- * flags) are mapped into the GPU lazily: the first call on a freshly
+ * through their UVA aliases.  0 disables.  Default 48 MiB: above it the
+ * copy-engine ring is faster (profiles/r01_ring_piece_sweep.jsonl: 32 MiB
+ * zero-copy 38.2 vs ring 36.7 GB/s, 64 MiB 39.2 vs 39.9).
+ * cudaHostRegister'ed buffers (default flags) are mapped into the GPU
+ * lazily: the first call on a freshly
  * registered buffer is slow (2 GB/s), later calls are not; register with
  * cudaHostRegisterMapped, or set 0, to avoid it. */
 int paes_cuda_set_zero_copy_max(uint64_t bytes);

@@ -48,7 +48,7 @@ std::vector<int> g_devices;  // empty = all visible
 // only for ranges beyond ~16 GiB; see there).
 std::uint64_t g_chunk = 256ull << 20;
 int g_streams = 3;
-std::atomic<std::uint64_t> g_zero_copy_max{128ull << 20};  // scripts/zero_copy_probe.cu
+std::atomic<std::uint64_t> g_zero_copy_max{48ull << 20};  // scripts/ring_piece_sweep.py: the ring wins from ~64 MiB
 
 int visible_devices() {
   int n = 0;
@@ -168,6 +168,10 @@ void ensure_pipeline(DevCtx& d, bool need_host) {
     for (auto p : d.dsc) cudaFree(p);
     for (auto s : d.st) cudaStreamDestroy(s);
     for (auto e : d.ev) cudaEventDestroy(e);
+    for (auto* v : {&d.ev_in, &d.ev_k, &d.ev_out}) {
+      for (auto e : *v) cudaEventDestroy(e);
+      v->clear();
+    }
     d.dbuf.clear();
     d.hbuf.clear();
     d.obuf.clear();
@@ -187,9 +191,11 @@ void ensure_pipeline(DevCtx& d, bool need_host) {
         cudaStream_t s;
         PAES_CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
         d.st.push_back(s);
-        cudaEvent_t e;
-        PAES_CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-        d.ev.push_back(e);
+        for (auto* v : {&d.ev, &d.ev_in, &d.ev_k, &d.ev_out}) {
+          cudaEvent_t e;
+          PAES_CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+          v->push_back(e);
+        }
         std::uint8_t* p = nullptr;
         PAES_CK(cudaMalloc(&p, chunk + 16));
         d.dbuf.push_back(p);
@@ -268,6 +274,19 @@ std::uint64_t piece_size(std::uint64_t len, std::uint64_t chunk, int streams) {
   if (p > kMid) p = std::max(kMid, len / 256);
   p = (p + 15) & ~std::uint64_t(15);
   return std::clamp(p, floor_piece, chunk);
+}
+
+// Piece size of the pinned direct ring (separate copy-in / kernel / copy-out
+// queues, run_host_range): ~16 pieces while they stay >= 8 MiB, at most
+// 64 MiB up to ~16 GiB, then len / 256 up to the slot.  Measured on 1x B200
+// (scripts/ring_piece_sweep.py, profiles/r01_ring_piece_sweep.jsonl): 256 MiB
+// 43.7 GB/s at 16 MiB pieces against 41.9 at the old len/6; 1 and 4 GiB best
+// at 32-64 MiB (46.2 / 47.8); pieces below 8 MiB lose ~19 us each.
+std::uint64_t pinned_piece_size(std::uint64_t len, std::uint64_t chunk) {
+  constexpr std::uint64_t kMin = 8ull << 20, kMid = 64ull << 20, kBig = 16ull << 30;
+  std::uint64_t p = len > kBig ? std::max(kMid, len / 256) : std::clamp(len / 16, kMin, kMid);
+  p = (p + 15) & ~std::uint64_t(15);
+  return std::clamp<std::uint64_t>(p, 16, chunk);
 }
 
 // Small host ranges (<= kSmallBytes): one memcpy into a mapped pinned buffer,
@@ -447,10 +466,19 @@ std::uint64_t run_host_range(DevCtx& d, const Range& r, const std::uint8_t* in, 
   if (!is_pinned(in) || !is_pinned(out)) return run_host_range_staged(d, r, in, out, kw);
   QuiesceOnThrow quiesce{d};
   const int S = static_cast<int>(d.st.size());
-  const std::uint64_t C = piece_size(r.in_len, d.chunk, S);
+  const std::uint64_t C = pinned_piece_size(r.in_len, d.chunk);
   const std::uint64_t npieces = std::max<std::uint64_t>(1, (r.in_len + C - 1) / C);
   // the last piece's trailer check writes the mapped status word directly
   if (r.check_pad) *reinterpret_cast<volatile std::uint32_t*>(d.h_status) = 0xffffffffu;  // unchecked => PaddingError
+  // One queue per engine: copy-in on st[0], kernels on st[1], copy-out on
+  // st[2] (roles wrap with fewer streams), events between them per slot.
+  // Piece k+S's copy-in waits only for piece k's copy-out (its slot), so the
+  // copy-in engine runs ahead and copy-out always has a piece queued; with
+  // all three steps of a piece on one stream, each kernel sat between its two
+  // copies and its launch/completion latency stalled the copy engines
+  // (scripts/ring_overhead_probe.cu, 1 GiB, empty kernel: 43.3 -> 45.0 GB/s at
+  // 8 MiB pieces, 46.2 -> 47.1 at 16 MiB).
+  cudaStream_t sin = d.st[0], sk = d.st[1 % S], sout = d.st[2 % S];
   std::uint64_t out_total = 0;
   for (std::uint64_t k = 0; k < npieces; ++k) {
     const int s = static_cast<int>(k % S);
@@ -458,10 +486,16 @@ std::uint64_t run_host_range(DevCtx& d, const Range& r, const std::uint8_t* in, 
     const std::uint64_t len = std::min<std::uint64_t>(C, r.in_len - off);
     const bool last = k + 1 == npieces;
     EcbArgs a = make_args(r, d.dbuf[s], d.dbuf[s], len, last, kw, d.m_status);
-    if (len) PAES_CK(copy_h2d_aligned(d.dbuf[s], in + off, len, d.st[s]));
-    PAES_CK(launch_ecb(r.dec, a, d.sm_count, d.st[s]));
+    if (k >= static_cast<std::uint64_t>(S)) PAES_CK(cudaStreamWaitEvent(sin, d.ev_out[s], 0));
+    if (len) PAES_CK(copy_h2d_aligned(d.dbuf[s], in + off, len, sin));
+    PAES_CK(cudaEventRecord(d.ev_in[s], sin));
+    PAES_CK(cudaStreamWaitEvent(sk, d.ev_in[s], 0));
+    PAES_CK(launch_ecb(r.dec, a, d.sm_count, sk));
+    PAES_CK(cudaEventRecord(d.ev_k[s], sk));
+    PAES_CK(cudaStreamWaitEvent(sout, d.ev_k[s], 0));
     const std::uint64_t olen = a.nblocks * 16;
-    if (olen) PAES_CK(copy_d2h_aligned(out + off, d.dbuf[s], olen, d.st[s]));
+    if (olen) PAES_CK(copy_d2h_aligned(out + off, d.dbuf[s], olen, sout));
+    PAES_CK(cudaEventRecord(d.ev_out[s], sout));
     out_total = off + olen;
   }
   for (auto s : d.st) PAES_CK(cudaStreamSynchronize(s));

@@ -86,6 +86,9 @@ struct DevCtx {
   std::vector<std::uint8_t*> dsc;   // [0]: the host batch's device descriptor image (all groups), lazy, grow-only
   std::vector<std::size_t> dsc_cap;
   std::vector<cudaEvent_t> ev;
+  // per slot, for the pinned ring's three queues: copy-in done, kernel done,
+  // copy-out done (slot free)
+  std::vector<cudaEvent_t> ev_in, ev_k, ev_out;
   std::uint64_t chunk = 0;
   std::uint32_t* h_status = nullptr;  // pinned, mapped; word 0 for host-pointer calls (d.mu held)
   std::uint32_t* m_status = nullptr;  // device alias of h_status: a one-shot check writes it directly

@@ -362,6 +362,9 @@ def csv_header() -> str:
     return CSV_HEADER
 
 
+DEFAULT_ZERO_COPY_MAX = 48 << 20  # the library's default (include/paes_cuda.h)
+
+
 def set_zero_copy_max(nbytes: int) -> None:
     """Pinned host ranges up to ``nbytes`` run as one zero-copy kernel on the
     caller's buffers (0 = always use the copy-engine ring)."""

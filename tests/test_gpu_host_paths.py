@@ -28,7 +28,7 @@ def test_ring_paths_vs_oracle(paes, gpu, orc, mode):
 
     pinned = mode != "pageable"
     paes.set_pipeline(64 * 1024, 3)  # tiny pieces: many slots in flight, small-path threshold 64 KiB
-    paes.set_zero_copy_max(0 if mode == "pinned_ring" else 128 * MiB)
+    paes.set_zero_copy_max(0 if mode == "pinned_ring" else paes.DEFAULT_ZERO_COPY_MAX)
     rnd = random.Random(hash(mode) & 0xFFFF)
     try:
         key = rnd.randbytes(16)
@@ -65,7 +65,7 @@ def test_ring_paths_vs_oracle(paes, gpu, orc, mode):
                 assert read(k) == expect
     finally:
         paes.set_pipeline(256 * MiB, 3)
-        paes.set_zero_copy_max(128 * MiB)
+        paes.set_zero_copy_max(paes.DEFAULT_ZERO_COPY_MAX)
 
 
 def test_oversized_pipeline_fails_cleanly_and_recovers(paes, gpu, orc):

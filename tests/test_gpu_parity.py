@@ -603,7 +603,7 @@ def test_multi_shard_pinned_zero_copy_and_ring(paes, gpu, orc):
     rk = paes.round_keys(key)
     paes.set_devices([0, 0, 0])
     try:
-        for zc in (128 << 20, 0):
+        for zc in (paes.DEFAULT_ZERO_COPY_MAX, 0):
             paes.set_zero_copy_max(zc)
             for n in (16 * 3 + 5, 1 << 20, (9 << 20) + 3):
                 data = rnd.randbytes(n)
@@ -617,5 +617,5 @@ def test_multi_shard_pinned_zero_copy_and_ring(paes, gpu, orc):
                 assert L.paes_cuda_chunk(1, dst.data_ptr(), olen.value, 1, rk, src.data_ptr(), C.byref(back), 3) == 0
                 assert back.value == n and src[:n].numpy().tobytes() == data, (zc, n)
     finally:
-        paes.set_zero_copy_max(128 << 20)
+        paes.set_zero_copy_max(paes.DEFAULT_ZERO_COPY_MAX)
         paes.set_devices([])
