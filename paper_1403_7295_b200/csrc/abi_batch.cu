@@ -388,23 +388,33 @@ int paes_cuda_batch_host(int dir, const uint8_t* h_in, uint8_t* h_out, const uin
       d.dsc_cap[0] = total;
     }
     std::uint8_t* const dimg = d.dsc[0];
-    PAES_CK(cudaMemcpyAsync(dimg, host, total, cudaMemcpyHostToDevice, d.st[0]));
-    PAES_CK(cudaEventRecord(d.ev[0], d.st[0]));
-    for (int i = 1; i < S; ++i) PAES_CK(cudaStreamWaitEvent(d.st[i], d.ev[0], 0));
+    // one queue per engine, as the pinned ring (runtime.cu run_host_range):
+    // copy-in on st[0], kernels on st[1], copy-out on st[2], per-slot events.
+    // Group k+S's copy-in reuses dbuf[slot] once group k's kernel has read
+    // it; its kernel reuses obuf[slot] once group k's copy-out is done.
+    cudaStream_t sin = d.st[0], sk = d.st[1 % S], sout = d.st[2 % S];
+    PAES_CK(cudaMemcpyAsync(dimg, host, total, cudaMemcpyHostToDevice, sin));  // ordered before every ev_in
     for (std::size_t k = 0; k < groups.size(); ++k) {
       const Group& g = groups[k];
       const BatchImage& b = imgs[k];
-      cudaStream_t s = d.st[k % S];
+      const int slot = static_cast<int>(k % S);
+      const bool reuse = k >= static_cast<std::size_t>(S);
       const bool fits = g.in_hi - g.in_lo <= cap + 16 && g.out_hi - g.out_lo <= cap + 16;
-      std::uint8_t* din = d.dbuf[k % S];
-      std::uint8_t* dout = d.obuf[k % S];
+      std::uint8_t* din = d.dbuf[slot];
+      std::uint8_t* dout = d.obuf[slot];
       std::uint8_t* dd = dimg + img_off[k];
+      if (reuse) PAES_CK(cudaStreamWaitEvent(sin, d.ev_k[slot], 0));
       if (!fits) {  // a single message larger than the staging chunk
-        PAES_CK(cudaMallocAsync(reinterpret_cast<void**>(&din), std::max<std::uint64_t>(16, g.in_hi - g.in_lo), s));
-        PAES_CK(cudaMallocAsync(reinterpret_cast<void**>(&dout), std::max<std::uint64_t>(16, g.out_hi - g.out_lo), s));
+        PAES_CK(cudaMallocAsync(reinterpret_cast<void**>(&din), std::max<std::uint64_t>(16, g.in_hi - g.in_lo), sin));
+        PAES_CK(cudaMallocAsync(reinterpret_cast<void**>(&dout), std::max<std::uint64_t>(16, g.out_hi - g.out_lo), sin));
       }
-      if (g.in_hi > g.in_lo) PAES_CK(copy_h2d_aligned(din, h_in + g.in_lo, g.in_hi - g.in_lo, s));
-      PAES_CK(launch_batch(b.dec, batch_args(b, din, dout, dd), d.sm_count, s));
+      if (g.in_hi > g.in_lo) PAES_CK(copy_h2d_aligned(din, h_in + g.in_lo, g.in_hi - g.in_lo, sin));
+      PAES_CK(cudaEventRecord(d.ev_in[slot], sin));
+      PAES_CK(cudaStreamWaitEvent(sk, d.ev_in[slot], 0));
+      if (reuse) PAES_CK(cudaStreamWaitEvent(sk, d.ev_out[slot], 0));
+      PAES_CK(launch_batch(b.dec, batch_args(b, din, dout, dd), d.sm_count, sk));
+      PAES_CK(cudaEventRecord(d.ev_k[slot], sk));
+      PAES_CK(cudaStreamWaitEvent(sout, d.ev_k[slot], 0));
       // copy back only the messages' output bytes, merged where they touch:
       // gaps between messages in h_out belong to the caller and are never
       // written (a packed layout such as config 5 is still one copy per group)
@@ -416,15 +426,16 @@ int paes_cuda_batch_host(int dir, const uint8_t* h_in, uint8_t* h_out, const uin
       for (std::size_t r = 0; r < rs.size();) {
         std::uint64_t lo = rs[r].first, hi = rs[r].second;
         for (++r; r < rs.size() && rs[r].first <= hi; ++r) hi = std::max(hi, rs[r].second);
-        PAES_CK(copy_d2h_aligned(h_out + lo, dout + (lo - g.out_lo), hi - lo, s));
+        PAES_CK(copy_d2h_aligned(h_out + lo, dout + (lo - g.out_lo), hi - lo, sout));
       }
       if (b.check)
         PAES_CK(cudaMemcpyAsync(host + img_off[k] + b.status_off, dd + b.status_off, 4ull * b.n,
-                                cudaMemcpyDeviceToHost, s));
+                                cudaMemcpyDeviceToHost, sout));
       if (!fits) {
-        PAES_CK(cudaFreeAsync(din, s));
-        PAES_CK(cudaFreeAsync(dout, s));
+        PAES_CK(cudaFreeAsync(din, sout));
+        PAES_CK(cudaFreeAsync(dout, sout));
       }
+      PAES_CK(cudaEventRecord(d.ev_out[slot], sout));
     }
     for (auto s : d.st) PAES_CK(cudaStreamSynchronize(s));
     PAES_CK(cudaEventRecord(t_stage.ev, d.st[0]));
