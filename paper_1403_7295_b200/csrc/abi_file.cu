@@ -97,7 +97,7 @@ void par_io(std::uint64_t n, unsigned threads, F&& f) {
     f(0, n);
     return;
   }
-  const std::uint64_t step = ((n / parts) + 4095) & ~std::uint64_t(4095);
+  const std::uint64_t step = (((n + parts - 1) / parts) + 4095) & ~std::uint64_t(4095);  // covers n
   std::vector<std::thread> pool;
   std::vector<std::string> errs(parts);
   for (std::uint64_t i = 1; i < parts; ++i) {

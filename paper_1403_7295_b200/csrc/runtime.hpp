@@ -6,11 +6,14 @@
 
 #include <cuda_runtime.h>
 
+#include <condition_variable>
 #include <cstdint>
 #include <exception>
+#include <memory>
 #include <mutex>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/paes_cuda.h"
@@ -73,6 +76,34 @@ class DeviceGuard {
   int prev_ = -1;
 };
 
+// ------------------------------------------------------------ host copy team
+// Persistent threads for parallel host memcpy (the staged ring copies every
+// piece in and out; a single core moves ~15 GB/s, and spawning a thread team
+// per piece cost ~0.5 ms per 10 MiB piece).  copy() is blocking and splits
+// the range over the team, the caller doing the first part; calls on one
+// team serialise.  Workers are bound to the device's NUMA node.
+class CopyTeam {
+ public:
+  CopyTeam(unsigned threads, int dev);
+  ~CopyTeam();
+  CopyTeam(const CopyTeam&) = delete;
+  CopyTeam& operator=(const CopyTeam&) = delete;
+  void copy(std::uint8_t* dst, const std::uint8_t* src, std::uint64_t n);
+
+ private:
+  void worker(unsigned idx, int dev);
+  std::mutex call_mu_;  // one copy() at a time
+  std::mutex mu_;
+  std::condition_variable go_, done_;
+  std::vector<std::thread> th_;
+  std::uint8_t* dst_ = nullptr;
+  const std::uint8_t* src_ = nullptr;
+  std::uint64_t n_ = 0, step_ = 0;
+  std::uint64_t gen_ = 0;
+  unsigned pending_ = 0;
+  bool stop_ = false;
+};
+
 // ------------------------------------------------------------ device context
 struct DevCtx {
   int id = -1;
@@ -82,6 +113,10 @@ struct DevCtx {
   std::vector<cudaStream_t> st;
   std::vector<std::uint8_t*> dbuf;  // chunk + 16 bytes each
   std::vector<std::uint8_t*> hbuf;  // pinned staging for the file path
+  // staged ring for pageable host buffers: pinned input and output slots
+  // (kStagedSlot bytes + 16 each) and one copy team per direction
+  std::vector<std::uint8_t*> sin_buf, sout_buf;
+  std::unique_ptr<CopyTeam> team_in, team_out;
   std::vector<std::uint8_t*> obuf;  // second device ring (batch output spans), chunk + 16 each, lazy
   std::vector<std::uint8_t*> dsc;   // [0]: the host batch's device descriptor image (all groups), lazy, grow-only
   std::vector<std::size_t> dsc_cap;
@@ -164,7 +199,6 @@ struct Range {
 EcbArgs make_args(const Range& r, const std::uint8_t* in, std::uint8_t* out, std::uint64_t in_len, bool last,
                   const KeyWords& kw, std::uint32_t* status);
 std::uint64_t piece_size(std::uint64_t len, std::uint64_t chunk, int streams);
-void par_copy(std::uint8_t* dst, const std::uint8_t* src, std::uint64_t n);
 // Host buffers on the device list: plan_chunks shards, one thread per shard.
 int host_transform(int dir, const std::uint8_t* in, std::uint64_t len, bool is_final, const std::uint8_t* rk,
                    std::uint8_t* out, std::uint64_t* out_len, int ngpus);

@@ -25,7 +25,7 @@ static double now() { return std::chrono::duration<double>(std::chrono::steady_c
 template <class F>
 static void par(unsigned t, std::size_t n, F f) {
   std::vector<std::thread> pool;
-  const std::size_t step = ((n / t) + 4095) & ~std::size_t(4095);
+  const std::size_t step = (((n + t - 1) / t) + 4095) & ~std::size_t(4095);
   for (unsigned i = 0; i < t; ++i) {
     const std::size_t b = std::min(n, i * step), e = std::min(n, (i + 1) * step);
     if (b < e) pool.emplace_back([=] { f(b, e - b); });

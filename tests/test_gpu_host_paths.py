@@ -119,3 +119,32 @@ def test_batch_host_messages_larger_than_the_staging_chunk(paes, gpu, orc):
         assert [back[o:o + n].tobytes() for o, n in zip(out_off, dl)] == msgs
     finally:
         paes.set_pipeline(256 * MiB, 3)
+
+
+def test_parallel_host_copies_cover_every_byte(paes, gpu, orc, tmp_path):
+    """Host copies split over T threads in 4 KiB-aligned parts: a length
+    n = T * 4096 * m + r (0 < r < T) once lost its last r bytes, because the
+    part size was rounded from floor(n / T).  Pageable lengths of that form
+    for the staged ring's copy teams (T = 8 on a 16-core box), and a file
+    whose last piece has that form for the file path's parallel I/O
+    (L = 6n + 75 gives 6 pieces of round16(n) .. n bytes, T = 2 parts)."""
+    key = bytes(range(16))
+    rnd = random.Random(4096)
+    for m in (40, 64, 100):
+        for r in (1, 5, 7):
+            n = 8 * 4096 * m + r
+            data = np.frombuffer(rnd.randbytes(n), dtype=np.uint8)
+            dst = np.zeros(n + 48, dtype=np.uint8)
+            k = _run(paes, 0, data.ctypes.data, n, True, key, dst.ctypes.data)
+            assert dst[:k].tobytes() == orc.encrypt_chunk(data.tobytes(), True, key), n
+            back = np.zeros(n + 48, dtype=np.uint8)
+            assert _run(paes, 1, dst.ctypes.data, k, True, key, back.ctypes.data) == n
+            assert back[:n].tobytes() == data.tobytes(), n
+    n_last = 2 * 4096 * 600 + 1
+    L = 6 * n_last + 75
+    data = rnd.randbytes(L)
+    (tmp_path / "p.bin").write_bytes(data)
+    paes.encrypt_file(str(tmp_path / "p.bin"), str(tmp_path / "c.bin"), key, workers=1)
+    assert (tmp_path / "c.bin").read_bytes() == orc.encrypt_chunk(data, True, key)
+    paes.decrypt_file(str(tmp_path / "c.bin"), str(tmp_path / "d.bin"), key, workers=1)
+    assert (tmp_path / "d.bin").read_bytes() == data
