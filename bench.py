@@ -530,7 +530,7 @@ def run_e2e(args, dist, paes, torch, pt, n, out_n, is_final, rk, dev):
     del host
     return {"value": round(tot * args.steps / el_max / 1e9, 3), "unit": "GB/s",
             "h2d_bytes_per_step": int(e_n), "d2h_bytes_per_step": int(olen.value),
-            "api": "paes_cuda_chunk (host pointers, pinned) -- 3 streams x 64-256 MiB H2D/kernel/D2H ring",
+            "api": "paes_cuda_chunk (host pointers, pinned) -- 3-slot ring with copy-in / kernel / copy-out on their own streams, len/256 pieces (256 MiB at 64 GiB)",
             "note": note, "ms_per_step": round(1e3 * el_max / args.steps, 3)}
 
 
