@@ -148,3 +148,31 @@ def test_parallel_host_copies_cover_every_byte(paes, gpu, orc, tmp_path):
     assert (tmp_path / "c.bin").read_bytes() == orc.encrypt_chunk(data, True, key)
     paes.decrypt_file(str(tmp_path / "c.bin"), str(tmp_path / "d.bin"), key, workers=1)
     assert (tmp_path / "d.bin").read_bytes() == data
+
+
+def test_staged_ring_large_pageable_matches_device_path(paes, gpu):
+    """The two-team staged ring over many 64 MiB pieces (pageable numpy
+    buffers, out of place and in place) against the device-resident path on
+    the same bytes, plus the decrypt round trip."""
+    import torch
+
+    key = bytes(range(3, 19))
+    rk = paes.round_keys(key)
+    for n in ((1 << 30) + 7, (192 << 20) + 3):
+        g = torch.Generator().manual_seed(n)
+        t = torch.randint(0, 256, (n,), dtype=torch.uint8, generator=g)
+        src = t.numpy()
+        m = (n // 16 + 1) * 16
+        d_in = t.cuda()
+        d_out = torch.empty(m + 16, dtype=torch.uint8, device="cuda")
+        assert paes.chunk_device(0, d_in.data_ptr(), n, True, rk, d_out.data_ptr()) == m
+        want = d_out[:m].cpu().numpy()
+        dst = np.zeros(m + 16, dtype=np.uint8)
+        assert _run(paes, 0, src.ctypes.data, n, True, key, dst.ctypes.data) == m
+        assert np.array_equal(dst[:m], want), n
+        inplace = np.zeros(m + 16, dtype=np.uint8)
+        inplace[:n] = src
+        assert _run(paes, 0, inplace.ctypes.data, n, True, key, inplace.ctypes.data) == m
+        assert np.array_equal(inplace[:m], want), n
+        assert _run(paes, 1, inplace.ctypes.data, m, True, key, inplace.ctypes.data) == n
+        assert np.array_equal(inplace[:n], src), n
