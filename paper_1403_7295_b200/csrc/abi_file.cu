@@ -5,6 +5,7 @@
 #include <fcntl.h>
 #include <sys/mman.h>
 #include <sys/stat.h>
+#include <sys/vfs.h>
 #include <unistd.h>
 
 #include <cerrno>
@@ -47,15 +48,30 @@ struct Map {
   }
 };
 
-// Size the output to `cap` and map it shared (plain pwrite if the file system
-// refuses mmap).  Its pages are allocated by the writer threads' own faults,
-// in parallel: preallocating with fallocate on a side thread was measured
-// slower (scripts/ab_file_variants.py, profiles/r01_file_prealloc_ab.json).
-// PAES_FILE_NO_MMAP=1 forces the pwrite path (file systems without shared
-// mmap take it on their own; the variable lets tests exercise it on tmpfs).
+// Size the output to `cap` and pick the writer by file system.  On tmpfs
+// (the paper's /dev/shm runs) the output is mapped shared and its pages are
+// allocated by the writer threads' own faults, in parallel: preallocating with
+// fallocate on a side thread was measured slower (scripts/ab_file_variants.py,
+// profiles/r01_file_prealloc_ab.json).  On disk file systems plain pwrite
+// from the pinned slots wins: 4 GiB on the box's ext4 root, 1.70 GB/s against
+// 1.27 with the mapping (ext4's page_mkwrite per faulted page;
+// profiles/r01_file_ext4_writer_ab.json).  File systems that refuse shared
+// mmap take pwrite too.  PAES_FILE_WRITER=mmap|pwrite overrides the choice
+// (tests exercise both); PAES_FILE_NO_MMAP=1 is the older spelling of pwrite.
 void open_output(int fd, std::uint64_t cap, Map& map) {
   if (!cap || ::ftruncate(fd, static_cast<off_t>(cap)) != 0) return;
-  if (const char* v = std::getenv("PAES_FILE_NO_MMAP"); v && v[0] == '1') return;
+  bool use_map;
+  const char* w = std::getenv("PAES_FILE_WRITER");
+  const char* nm = std::getenv("PAES_FILE_NO_MMAP");
+  if (w && std::strcmp(w, "mmap") == 0) {
+    use_map = true;
+  } else if ((w && std::strcmp(w, "pwrite") == 0) || (nm && nm[0] == '1')) {
+    use_map = false;
+  } else {
+    struct statfs fs {};
+    use_map = ::fstatfs(fd, &fs) == 0 && static_cast<unsigned long>(fs.f_type) == 0x01021994ul;  // TMPFS_MAGIC
+  }
+  if (!use_map) return;
   void* p = ::mmap(nullptr, cap, PROT_READ | PROT_WRITE, MAP_SHARED, fd, 0);
   if (p != MAP_FAILED) {
     map.p = static_cast<std::uint8_t*>(p);

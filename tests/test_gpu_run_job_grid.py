@@ -83,12 +83,18 @@ def test_acceptance_roundtrip_200_files(paes, gpu, ref, eight_workers, tmp_path)
         assert rc == 0 and back.read_bytes() == data, (i, size)
 
 
-@pytest.mark.parametrize("no_mmap", ["0", "1"])
-def test_large_file_parallel_io_and_pwrite_path(paes, gpu, ref, eight_workers, tmp_path, monkeypatch, no_mmap):
+@pytest.mark.parametrize("writer", ["mmap", "pwrite", "auto", "no_mmap_env"])
+def test_large_file_parallel_io_and_pwrite_path(paes, gpu, ref, eight_workers, tmp_path, monkeypatch, writer):
     """A file large enough that pread / write-back split across I/O threads
-    (pieces > 4 MiB), through the shared-mapping writer and (PAES_FILE_NO_MMAP=1)
-    the pwrite fallback; byte-identical to the reference's run_job."""
-    monkeypatch.setenv("PAES_FILE_NO_MMAP", no_mmap)
+    (pieces > 4 MiB), through the shared-mapping writer, the pwrite writer,
+    the file system's default (tmpfs: mapping, disk: pwrite) and the older
+    PAES_FILE_NO_MMAP=1 switch; byte-identical to the reference's run_job."""
+    monkeypatch.delenv("PAES_FILE_WRITER", raising=False)
+    monkeypatch.delenv("PAES_FILE_NO_MMAP", raising=False)
+    if writer in ("mmap", "pwrite"):
+        monkeypatch.setenv("PAES_FILE_WRITER", writer)
+    elif writer == "no_mmap_env":
+        monkeypatch.setenv("PAES_FILE_NO_MMAP", "1")
     rnd = random.Random(909)
     key = rnd.randbytes(16)
     src = tmp_path / "big.bin"
