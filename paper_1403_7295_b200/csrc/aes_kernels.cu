@@ -18,6 +18,14 @@ std::atomic<unsigned long long> g_launches{0};
 
 namespace {
 
+// Programmatic dependent launch for ecb_kernel (PAES_PDL=0 builds plain
+// launches): measured on queued C launches (scripts/mid_launch_probe.cu,
+// profiles/r01_pdl_ab.json) 16 MiB 703 -> 786 GB/s, 64 MiB 819 -> 848,
+// 1 GiB 869 -> 870; a single launch loses the first-tile prefetch that used
+// to hide behind the table staging (0-2 %).
+#ifndef PAES_PDL
+#define PAES_PDL 1
+#endif
 #ifndef PAES_THREADS
 #define PAES_THREADS 512
 #endif
@@ -304,9 +312,20 @@ __global__ void __launch_bounds__(kThreads, 1) ecb_kernel(const __grid_constant_
 #pragma unroll
     for (int j = 0; j < NB; ++j) nxt[j] = load_block<ALIGNED>(a.in + 16ull * (t * kTile + lane + 32ull * j));
   };
+#if PAES_PDL
+  // programmatic dependent launch: stage the tables (constant data) while the
+  // previous kernel in the stream drains, let the next launch in, and touch
+  // the buffers only once the previous grid has completed
+  stage_tables<DEC>(sm);
+  asm volatile("griddepcontrol.launch_dependents;");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  if (tile < full_tiles) load_tile(tile);
+  __syncthreads();
+#else
   if (tile < full_tiles) load_tile(tile);
   stage_tables<DEC>(sm);
   __syncthreads();
+#endif
   const char* smb = reinterpret_cast<const char*>(sm);
   for (; tile < full_tiles; tile += tstride) {
     const unsigned long long b0 = tile * kTile + lane;
@@ -601,6 +620,24 @@ cudaError_t launch_ecb(bool dec, const EcbArgs& args, int sm_count, cudaStream_t
   clear_stale_error();
   const bool aligned = ((reinterpret_cast<std::uintptr_t>(args.in) | reinterpret_cast<std::uintptr_t>(args.out)) & 15) == 0;
   const int smem = dec ? kDecLaunchSmem : kEncLaunchSmem;
+#if PAES_PDL
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(static_cast<unsigned>(grid));
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = static_cast<std::size_t>(smem);
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaError_t le;
+  if (dec) le = aligned ? cudaLaunchKernelEx(&cfg, ecb_kernel<true, kNB, true>, args)
+                        : cudaLaunchKernelEx(&cfg, ecb_kernel<true, kNB, false>, args);
+  else le = aligned ? cudaLaunchKernelEx(&cfg, ecb_kernel<false, kNB, true>, args)
+                    : cudaLaunchKernelEx(&cfg, ecb_kernel<false, kNB, false>, args);
+  if (le != cudaSuccess) return le;
+#else
   if (dec) {
     if (aligned) ecb_kernel<true, kNB, true><<<static_cast<unsigned>(grid), kThreads, smem, stream>>>(args);
     else ecb_kernel<true, kNB, false><<<static_cast<unsigned>(grid), kThreads, smem, stream>>>(args);
@@ -608,6 +645,7 @@ cudaError_t launch_ecb(bool dec, const EcbArgs& args, int sm_count, cudaStream_t
     if (aligned) ecb_kernel<false, kNB, true><<<static_cast<unsigned>(grid), kThreads, smem, stream>>>(args);
     else ecb_kernel<false, kNB, false><<<static_cast<unsigned>(grid), kThreads, smem, stream>>>(args);
   }
+#endif
   g_launches.fetch_add(1, std::memory_order_relaxed);
   return cudaGetLastError();
 }
