@@ -298,9 +298,11 @@ __global__ void __launch_bounds__(kThreads, 1) ecb_kernel(const __grid_constant_
   // The next tile's blocks are loaded before the current tile is computed
   // (register double buffer), so a warp never waits on HBM at a tile start --
   // otherwise the SM's warps, which advance in near lockstep on short
-  // launches, all stall on the same load latency together.  The first tile's
-  // loads are issued before the tables are staged, so their HBM latency hides
-  // behind the staging (this is most of a small launch's duration).
+  // launches, all stall on the same load latency together.  Without PDL the
+  // first tile's loads are issued before the tables are staged, so their HBM
+  // latency hides behind the staging; with PDL (the default) the staging
+  // instead overlaps the previous launch's tail, and the loads wait for
+  // griddepcontrol.wait.
   // Full tiles keep all 32 lanes active, so an output that is not even
   // 4-byte aligned is written by whole rows (store_row_unaligned).  Measured
   // on 1 GiB (scripts/unaligned_probe.py): per-lane double-chunk loads + word
