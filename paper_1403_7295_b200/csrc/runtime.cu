@@ -263,13 +263,13 @@ EcbArgs make_args(const Range& r, const std::uint8_t* in, std::uint8_t* out, std
   return a;
 }
 
-// Piece size for a range, from measurements on the box (pinned and staged
-// paths, in and out of place; scripts/e2e_ring_sweep.py, pcie_probe.py,
-// pageable_probe.py):
+// Piece size of the file path (abi_file.cu) and the host batch groups
+// (abi_batch.cu), from measurements on the box (scripts/e2e_ring_sweep.py,
+// pcie_probe.py, batch_host_probe.py); the pinned and staged rings have their
+// own (pinned_piece_size, staged_piece_size):
 // - short ranges: ~2 pieces per stream so copy-in, kernel and copy-out overlap;
 // - up to ~16 GiB: 64 MiB pieces (1 GiB: 46.1 GB/s at 64 MiB against 44.6 at
-//   both 33 MB and 128 MiB; smaller pieces also cost the staged path its copy
-//   threads' spawn per piece);
+//   both 33 MB and 128 MiB);
 // - beyond: len / 256, up to the ring slot (64 GiB in place: 49.3 GB/s at
 //   256 MiB against 48.3 at 64 MiB -- fewer per-piece gaps).
 std::uint64_t piece_size(std::uint64_t len, std::uint64_t chunk, int streams) {
