@@ -619,3 +619,39 @@ def test_multi_shard_pinned_zero_copy_and_ring(paes, gpu, orc):
     finally:
         paes.set_zero_copy_max(paes.DEFAULT_ZERO_COPY_MAX)
         paes.set_devices([])
+
+
+def test_sharded_pageable_staged_ring_and_tmpfs_writer(paes, gpu, orc, tmp_path):
+    """Pageable buffers large enough for the staged ring, sharded over a
+    three-entry device list (three shard threads, one device, its copy teams
+    shared under the device lock); and run_job's default writer on tmpfs
+    (/dev/shm: the shared mapping) as well as on tmp_path's file system."""
+    rnd = random.Random(5150)
+    key = rnd.randbytes(16)
+    paes.set_devices([0, 0, 0])
+    try:
+        for n in ((12 << 20) + 5, (30 << 20) + 16):
+            data = rnd.randbytes(n)
+            ct = paes.encrypt_chunk(data, True, key, ngpus=3)
+            assert ct == orc.encrypt_chunk(data, True, key, threads=4), n
+            assert paes.decrypt_chunk(ct, True, key, ngpus=3) == data, n
+    finally:
+        paes.set_devices([])
+    data = rnd.randbytes((9 << 20) + 3)
+    want = orc.encrypt_chunk(data, True, key, threads=4)
+    dirs = [str(tmp_path)] + (["/dev/shm"] if os.path.isdir("/dev/shm") and os.access("/dev/shm", os.W_OK) else [])
+    for d in dirs:
+        src, dst, back = (os.path.join(d, f"paes_t{os.getpid()}_{x}") for x in ("p", "c", "d"))
+        try:
+            with open(src, "wb") as f:
+                f.write(data)
+            paes.encrypt_file(src, dst, key, workers=1)
+            with open(dst, "rb") as f:
+                assert f.read() == want, d
+            paes.decrypt_file(dst, back, key, workers=1)
+            with open(back, "rb") as f:
+                assert f.read() == data, d
+        finally:
+            for p in (src, dst, back):
+                if os.path.exists(p):
+                    os.unlink(p)
