@@ -4,7 +4,7 @@
 set -u
 mkdir -p gpurun_out
 : > gpurun_out/campaign_summary.txt
-for seed in 11 12 13 14 15 16 17 18; do
+for seed in ${FUZZ_SEEDS:-11 12 13 14 15 16 17 18}; do
   PAES_FUZZ_SCALE=40 PAES_FUZZ_SEED=$seed timeout 900 python -m pytest tests/test_gpu_fuzz.py -m gpu -x -q > gpurun_out/campaign_$seed.log 2>&1
   echo "fuzz seed=$seed scale=40 rc=$? $(tail -1 gpurun_out/campaign_$seed.log)" >> gpurun_out/campaign_summary.txt
 done
