@@ -237,10 +237,10 @@ def reference_sample(total_bytes: int, seed: int, target_s: float):
     return R, key, pt, ct, logical, phys
 
 
-def run_reference(args, dist: Dist):
+def run_reference(args, rank: int):
     """`--impl reference`: the reference's pthreads path (exec.cpp:143-202 minus
     file I/O) on all host threads, rank 0 only."""
-    if dist.rank != 0:
+    if rank != 0:
         return None
     R, key, pt, ct, workers, phys = reference_sample(args.total_bytes, args.seed, target_s=args.ref_step_s)
     for _ in range(args.warmup):
@@ -563,15 +563,19 @@ def main():
     # PAES_BENCH_SHARED_DEVICE=1: every rank on cuda:0 over gloo -- a plumbing
     # smoke of the N>1 path on a one-GPU box (ranks never wait on each other's
     # kernels; only CPU barriers and scalar reductions cross ranks).
+    if args.impl == "reference":
+        # CPU only and rank 0 only: no process group, no CUDA (the other ranks
+        # of a torchrun launch exit 0 at once)
+        res = run_reference(args, env_int("RANK", 0))
+        if res is not None:
+            print(json.dumps(res), flush=True)
+        return
     shared = os.environ.get("PAES_BENCH_SHARED_DEVICE") == "1"
     dist = Dist(args.gpus, backend="gloo" if shared else "nccl")
     try:
-        if args.impl == "reference":
-            res = run_reference(args, dist)
-        else:
-            res = run_b200(args, dist)
-            if res is not None and dist.rank == 0 and dist.world == 1 and not args.no_cpu:
-                res["cpu_baseline"] = cpu_baseline(args)
+        res = run_b200(args, dist)
+        if res is not None and dist.rank == 0 and dist.world == 1 and not args.no_cpu:
+            res["cpu_baseline"] = cpu_baseline(args)
         if res is not None and dist.rank == 0:
             print(json.dumps(res), flush=True)
     finally:
