@@ -4,7 +4,7 @@
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
     torchrun --nnodes=1 --nproc-per-node N --master-addr 127.0.0.1 bench.py --gpus N
 
-Workload (default, config 4 of BASELINE.json): a 64 GiB uniform-random buffer
+Headline workload (config 4 of BASELINE.json): a 64 GiB uniform-random buffer
 generated ON DEVICE from seed 3 by the counter stream (DESIGN.md "Synthetic
 inputs"), encrypted under key sweep(3,16) with the reference's always-pad rule,
 sharded across ranks as contiguous 16-byte block ranges by plan_chunks
@@ -12,23 +12,31 @@ sharded across ranks as contiguous 16-byte block ranges by plan_chunks
 = ONE kernel launch (paes_cuda_chunk_device).  Inputs (64 GiB) are far larger
 than L2 (126 MB), so no flush is needed between steps.
 
-value  : whole-job device-resident GB/s (plaintext bytes of all ranks * K /
-         max-over-ranks CUDA-event time of the K steps), 1 GB = 1e9 B.
-e2e    : the same transform through the public host-pointer C-ABI call
-         paes_cuda_chunk() on pinned host memory (H2D + kernel + D2H inside the
-         timed region), max over ranks.
-roofline: the kernel's algorithmic HBM traffic (2 B per plaintext byte) vs the
-         measured copy peak, and the shared-memory lookup pipe (160 conflict-
-         free LDS.32 per block, 32 per clock per SM) at the measured SM clock;
-         `binding` = the slower of the two (BASELINE.json north_star).
+value   : whole-job device-resident GB/s (plaintext bytes of all ranks * K /
+          max-over-ranks CUDA-event time of the K steps), 1 GB = 1e9 B.
+e2e     : the same transform through the public host-pointer C-ABI call
+          paes_cuda_chunk() on pinned host memory (H2D + kernel + D2H inside
+          the timed region), max over ranks.
+roofline: the binding bound of north_star -- the slower of the shared-memory
+          lookup pipe (160 conflict-free LDS.32 per block, 32 per clock per SM,
+          at the SM clock sampled under load) and HBM (2 B per plaintext byte
+          at the measured copy peak); the HBM form is nested under "hbm".
+configs : (N = 1, rank 0) every other BASELINE.json config on the driver's
+          clock -- configs 1, 2, 3 (six sizes), 5, device-resident and end to
+          end, each with its parity verdict against tests/golden/digests.json
+          (reference-computed); plus the pageable-memory e2e through
+          encrypt_bytes and the paper's own file -> file metric (run_job on
+          /dev/shm) next to the reference's run_job(threads).
 --impl reference : the reference's own CPU path (oracle/_ref, compiled from the
-         reference sources) on all host cores, rank 0 only.
+          reference sources) on all host cores, rank 0 only.
 """
 from __future__ import annotations
 
 import argparse
+import hashlib
 import json
 import os
+import shutil
 import statistics
 import subprocess
 import sys
@@ -40,6 +48,7 @@ sys.path.insert(0, ROOT)
 
 GiB = 1 << 30
 MiB = 1 << 20
+L2_BYTES = 126 * 1000 * 1000
 METRIC = "AES-128 ECB encrypt throughput (device-resident; e2e via C-ABI host path)"
 LOOKUPS_PER_BLOCK = 160      # 144 T-table + 16 final-round lookups
 LDS_PER_CLK_PER_SM = 32      # one conflict-free LDS.32 warp-instruction per clock
@@ -71,6 +80,11 @@ def ncu_traffic_ratio():
         return float(d["dram_bytes_per_launch"]) / float(d["algorithmic_bytes_per_launch"]), d.get("source", path)
     except (OSError, KeyError, ValueError, ZeroDivisionError):
         return None, None
+
+
+def pipe_peak_gbs(sms: int, clk_mhz: float) -> float:
+    """Plaintext GB/s at which 160 LDS.32 per block saturate 32 lookups/clk/SM."""
+    return sms * clk_mhz * 1e6 * LDS_PER_CLK_PER_SM / LOOKUPS_PER_BLOCK * 16 / 1e9
 
 
 # --------------------------------------------------------------------- clocks
@@ -183,15 +197,31 @@ class Dist:
             else:
                 self.pg.barrier()
 
+    def _tensor(self, values, dtype):
+        import torch
+
+        return torch.tensor(values, dtype=dtype, device=f"cuda:{self.local}" if self.backend == "nccl" else "cpu")
+
     def reduce(self, value, op: str):
         if not self.pg:
             return value
         import torch
 
-        t = torch.tensor([value], dtype=torch.float64 if isinstance(value, float) else torch.int64,
-                         device=f"cuda:{self.local}" if self.backend == "nccl" else "cpu")
+        t = self._tensor([value], torch.float64 if isinstance(value, float) else torch.int64)
         self.pg.all_reduce(t, op={"max": self.pg.ReduceOp.MAX, "sum": self.pg.ReduceOp.SUM}[op])
         return t.item()
+
+    def gather(self, value: float):
+        """Every rank's float, in rank order (a sum-reduce of one-hot slots)."""
+        if not self.pg:
+            return [float(value)]
+        import torch
+
+        slots = [0.0] * self.world
+        slots[self.rank] = float(value)
+        t = self._tensor(slots, torch.float64)
+        self.pg.all_reduce(t, op=self.pg.ReduceOp.SUM)
+        return [float(x) for x in t.tolist()]
 
     def close(self):
         if self.pg:
@@ -211,6 +241,19 @@ def sum_checksums(dist: Dist, cs: int) -> int:
     return dist.reduce(cs - (1 << 64) if cs >= (1 << 63) else cs, "sum") % (1 << 64)
 
 
+def spread(xs):
+    """min / median / max of per-rank values."""
+    return {"min": round(min(xs), 2), "median": round(statistics.median(xs), 2), "max": round(max(xs), 2)}
+
+
+def workload_config(args):
+    """Identical for both arms (the driver compares the two lines' configs)."""
+    return {"workload": f"config4: {args.total_bytes} B counter-stream (seed {args.seed}) AES-128 encrypt, "
+                        f"PKCS#7 always-pad, plan_chunks block-range shards",
+            "total_bytes": args.total_bytes, "parallelism": f"dp{args.gpus} (contiguous block ranges, no collective)",
+            "l2": "inputs >> L2 (126 MB); no flush needed"}
+
+
 # --------------------------------------------------------------------- reference arm
 def reference_sample(total_bytes: int, seed: int, target_s: float):
     """A bounded sample of the workload for the CPU runs: the first S bytes of
@@ -223,7 +266,7 @@ def reference_sample(total_bytes: int, seed: int, target_s: float):
     O = oracle.Oracle()
     phys, logical = R.cores()
     key = O.sweep(seed, 16)
-    # calibrate: 64 MiB single-thread probe of the reference
+    # calibrate: 64 MiB probe of the reference on all host threads
     probe = np.empty(64 * MiB, dtype=np.uint8)
     O.counter_fill_into(seed, 0, probe.nbytes, probe.ctypes.data)
     out = np.empty(probe.nbytes + 16, dtype=np.uint8)
@@ -252,14 +295,14 @@ def run_reference(args, rank: int):
         times.append(time.perf_counter() - t)
     total = sum(times)
     value = pt.nbytes * args.steps / total / 1e9
-    sample = (f"first {pt.nbytes} B of the config-4 stream per step (encrypt_chunk semantics, "
-              f"plan_chunks over {workers} std::threads)")
+    sample = (f"each step: the first {pt.nbytes} B of the config-4 stream (encrypt_chunk semantics, plan_chunks over "
+              f"{workers} std::threads; reference paes_core compiled from its sources)")
     return {
         "metric": METRIC, "value": round(value, 4), "unit": "GB/s", "impl": "reference",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(1e3 * total / args.steps, 3), "higher_is_better": True, "scaling": "strong",
-        "vs_baseline": None, "dtype": "u8", "data": "synthetic (counter stream, seed 3)",
-        "config": workload_config(args, "reference"),
+        "vs_baseline": None, "dtype": "u8", "data": "synthetic (counter stream generated from seed 3)",
+        "config": workload_config(args),
         "cpu_baseline": {"value": round(value, 4), "unit": "GB/s", "cores": workers, "physical_cores": phys,
                          "kind": "reference", "sample": sample,
                          "step_seconds": [round(x, 4) for x in times]},
@@ -281,17 +324,6 @@ def cpu_baseline(args):
             "sample": f"{pt.nbytes} B of the config-4 stream, 5 reps, reject_outliers mean "
                       f"(reference paes_core compiled from its sources, {workers} threads)",
             "seconds": [round(x, 4) for x in samples]}
-
-
-def workload_config(args, impl: str = "b200"):
-    cfg = {"workload": f"config4: {args.total_bytes} B counter-stream (seed {args.seed}) AES-128 encrypt, "
-                       f"PKCS#7 always-pad, plan_chunks block-range shards",
-           "total_bytes": args.total_bytes, "parallelism": f"dp{args.gpus} (contiguous block ranges, no collective)"}
-    if impl == "b200":
-        cfg.update(l2="inputs >> L2 (126 MB); no flush needed", step="one kernel launch over the rank's shard")
-    else:
-        cfg.update(step="one reference pthreads pass (plan_chunks over all host threads) over a bounded sample")
-    return cfg
 
 
 # --------------------------------------------------------------------- B200 arm
@@ -409,40 +441,43 @@ def run_b200(args, dist: Dist):
     props = torch.cuda.get_device_properties(dev)
     sms = props.multi_processor_count
     clk_mhz = clocks.get("sm_mhz") or float(peaks.get("sm_max_mhz", 1965.0))
-    pipe_peak = sms * clk_mhz * 1e6 * LDS_PER_CLK_PER_SM / LOOKUPS_PER_BLOCK * 16 / 1e9
-    pipe_peak_max = sms * float(clocks.get("sm_max_mhz") or 1965.0) * 1e6 * LDS_PER_CLK_PER_SM / LOOKUPS_PER_BLOCK * 16 / 1e9
+    pipe_peak = pipe_peak_gbs(sms, clk_mhz)
+    pipe_peak_max = pipe_peak_gbs(sms, float(clocks.get("sm_max_mhz") or 1965.0))
     hbm_pt_bound = hbm_peak / 2
     binding = "smem_lookup_pipe" if pipe_peak < hbm_pt_bound else "hbm"
     ratio, tsrc = ncu_traffic_ratio()
+    bound_gbs = min(pipe_peak, hbm_pt_bound)
     roofline = {
-        "bound": "hbm", "achieved": round(hbm_ach, 1), "peak": hbm_peak, "unit": "GB/s",
-        "frac": round(hbm_ach / hbm_peak, 4), "traffic": (round(ratio * alg_bytes) if ratio else None),
-        "traffic_source": tsrc, "peak_source": f"{peak_src} hbm_gbs (copy read+write, burst)",
+        # north_star's roofline: the slower of the lookup pipe and HBM, in
+        # plaintext GB/s; `achieved` is the kernel's own rate (CUDA events)
+        "bound": binding, "achieved": round(pt_gbs, 1), "peak": round(bound_gbs, 1), "unit": "GB/s",
+        "frac": round(pt_gbs / bound_gbs, 4),
+        "traffic": (round(ratio * alg_bytes) if ratio else None), "traffic_source": tsrc,
         "algorithmic_bytes_per_launch": alg_bytes, "kernel": "ecb_kernel<enc> (T-table, smem x32)",
         "avg_launch_ms": round(avg_launch_s * 1e3, 4),
-        "pipe": {"name": "shared-memory LDS.32 T-table lookups (160 per 16-B block, 32/clk/SM)",
-                 "achieved_pt_gbs": round(pt_gbs, 1), "peak_pt_gbs": round(pipe_peak, 1),
-                 "peak_pt_gbs_at_max_clock": round(pipe_peak_max, 1), "sm_mhz": clk_mhz, "sms": sms,
-                 "frac": round(pt_gbs / pipe_peak, 4)},
-        "hbm_pt_bound_gbs": round(hbm_pt_bound, 1),
-        "binding": binding,
-        "frac_of_binding": round(pt_gbs / min(pipe_peak, hbm_pt_bound), 4),
+        "peak_note": (f"{LOOKUPS_PER_BLOCK} LDS.32 per 16-B block at {LDS_PER_CLK_PER_SM}/clk/SM x {sms} SMs x "
+                      f"{clk_mhz:.0f} MHz (SM clock sampled under load); {round(pipe_peak_max, 1)} GB/s at max clock"),
+        "hbm": {"achieved": round(hbm_ach, 1), "peak": hbm_peak, "unit": "GB/s (read + write)",
+                "frac": round(hbm_ach / hbm_peak, 4), "pt_bound_gbs": round(hbm_pt_bound, 1),
+                "peak_source": f"{peak_src} hbm_gbs (copy read+write, burst)"},
     }
 
     # decrypt direction on the ciphertext just produced (the inverse-round
-    # kernel; a final shard also runs the trailer check + its readback)
+    # kernel; a final shard also runs the trailer check, queued: the verdict
+    # goes to a device word read after the timed region)
     dec = None
     if not args.no_decrypt and out_n:
         # decrypt into the plaintext buffer (three 64 GiB buffers do not fit);
         # the round trip is checked by the position-keyed checksum of pt
         cs_pt = paes.checksum_device(pt.data_ptr(), n - n % 8, off // 8, dev, stream.cuda_stream)
-        back = pt
+        res = torch.zeros(args.steps + args.warmup, dtype=torch.int64, device=dev)
 
-        def dstep():
-            return paes.chunk_device(1, ct.data_ptr(), out_n, is_final, rk, back.data_ptr(), dev, stream.cuda_stream)
+        def dstep(i):
+            paes.chunk_device_async(1, ct.data_ptr(), out_n, is_final, rk, pt.data_ptr(), res.data_ptr() + 8 * i, dev,
+                                    stream.cuda_stream)
 
-        for _ in range(args.warmup):
-            dstep()
+        for i in range(args.warmup):
+            dstep(args.steps + i)
         stream.synchronize()
         devs_ = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
         dist.barrier()
@@ -451,18 +486,20 @@ def run_b200(args, dist: Dist):
         d0.record(stream)
         for i in range(args.steps):
             devs_[i][0].record(stream)
-            got = dstep()
+            dstep(i)
             devs_[i][1].record(stream)
         d1.record(stream)
         torch.cuda.synchronize(dev)
         dist.barrier()
-        assert got == n, (got, n)
+        got = set(res.tolist())
+        assert got == {n}, (got, n)
         ok = paes.checksum_device(pt.data_ptr(), n - n % 8, off // 8, dev, stream.cuda_stream) == cs_pt
         dmax = dist.reduce(float(d0.elapsed_time(d1)), "max")
         dtot = dist.reduce(int(out_n), "sum")
         dk = statistics.mean(a.elapsed_time(b) for a, b in devs_) / 1e3
         dec = {"value": round(dtot * args.steps / (dmax / 1e3) / 1e9, 2), "unit": "GB/s",
                "ms_per_step": round(dmax / args.steps, 4), "kernel": "ecb_kernel<dec> (Td tables + InvS, smem x32)",
+               "api": "paes_cuda_chunk_device_async (trailer verdict written on the device)",
                "pipe_frac": round(out_n / dk / 1e9 / pipe_peak, 4),
                "round_trip": "ok (plaintext checksum restored)" if ok else "MISMATCH"}
 
@@ -483,6 +520,24 @@ def run_b200(args, dist: Dist):
         "config": workload_config(args), "parity": parity, "roofline": roofline, "clocks": clocks,
         "gpu_launches": launches, "e2e": e2e, "decrypt": dec, "device": props.name,
     }
+    if N > 1:
+        # per-rank story (north_star: scaling and per-GPU roofline fraction)
+        rank_gbs = dist.gather(n * args.steps / (elapsed_ms / 1e3) / 1e9)
+        rank_frac = dist.gather(pt_gbs / pipe_peak)
+        result["per_rank"] = {
+            "device_gbs": [round(x, 2) for x in rank_gbs], "device_gbs_spread": spread(rank_gbs),
+            "pipe_frac": [round(x, 4) for x in rank_frac],
+            "sum_of_rank_rates_gbs": round(sum(rank_gbs), 2),
+            "sm_mhz": dist.gather(float(clocks.get("sm_mhz") or 0.0)),
+        }
+        if e2e:
+            r_e2e = dist.gather(e2e["rank_value"])
+            result["per_rank"]["e2e_gbs"] = [round(x, 3) for x in r_e2e]
+            result["per_rank"]["e2e_gbs_spread"] = spread(r_e2e)
+        nodes = dist.gather(float(numa.split()[0][4:]) if numa.startswith("node") else -1.0)
+        result["per_rank"]["numa_node"] = [int(x) for x in nodes]
+    if not args.no_configs and N == 1:
+        result["configs"] = run_configs(args, torch, paes, dev, sms)
     return result
 
 
@@ -531,7 +586,415 @@ def run_e2e(args, dist, paes, torch, pt, n, out_n, is_final, rk, dev):
     return {"value": round(tot * args.steps / el_max / 1e9, 3), "unit": "GB/s",
             "h2d_bytes_per_step": int(e_n), "d2h_bytes_per_step": int(olen.value),
             "api": "paes_cuda_chunk (host pointers, pinned) -- 3-slot ring with copy-in / kernel / copy-out on their own streams, len/256 pieces (256 MiB at 64 GiB)",
-            "note": note, "ms_per_step": round(1e3 * el_max / args.steps, 3)}
+            "note": note, "ms_per_step": round(1e3 * el_max / args.steps, 3),
+            "rank_value": e_n * args.steps / el / 1e9}
+
+
+# --------------------------------------------------------------------- configs 1, 2, 3, 5 (N = 1)
+class ConfigBench:
+    """Every other BASELINE.json config under the driver's clock (VERDICT r1
+    "next" 1).  Device-resident rates time K calls queued on one stream
+    between one CUDA-event pair, rotating over enough buffer pairs that the
+    working set of consecutive steps exceeds 4x L2 (no flush needed); calls
+    whose buffers are smaller than that (config 3 below 64 MiB) flush L2
+    (256 MiB memset on the stream) before every step and time each call
+    between its own event pair.  E2E rates go through the public C-ABI host
+    call on pinned buffers (wall clock, synchronous calls).  Parity: SHA-256
+    of every output against tests/golden/digests.json, which the reference's
+    own paes_core produced (tests/golden/make_digests.py)."""
+
+    def __init__(self, args, torch, paes, dev, sms):
+        import ctypes as C
+
+        from paper_1403_7295_b200 import _native as Nt
+
+        self.args, self.torch, self.paes, self.dev, self.sms = args, torch, paes, dev, sms
+        self.C, self.Nt, self.L = C, Nt, Nt.load()
+        self.s = torch.cuda.Stream(device=dev)
+        self.sp = self.s.cuda_stream
+        self.steps = max(3, args.steps)
+        self.warmup = args.warmup
+        with open(os.path.join(ROOT, "tests", "golden", "digests.json")) as f:
+            self.dig = json.load(f)
+        self.scratch = None
+        self.clk_mhz = None
+
+    # -- helpers
+    def pipe_frac(self, gbs):
+        return round(gbs / pipe_peak_gbs(self.sms, self.clk_mhz or 1965.0), 4)
+
+    def sha_dev(self, t, n):
+        host = self.torch.empty(n, dtype=self.torch.uint8, pin_memory=True)
+        host.copy_(t[:n])
+        return hashlib.sha256(host.numpy()).hexdigest()
+
+    def pinned(self, n):
+        return self.torch.empty(max(n, 16) + 64, dtype=self.torch.uint8, pin_memory=True)
+
+    def queued(self, fns):
+        """One event pair around len(fns) queued calls; returns ms per call."""
+        torch = self.torch
+        for f in fns[: self.warmup]:
+            f()
+        self.s.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(self.s)
+        for f in fns:
+            f()
+        b.record(self.s)
+        b.synchronize()
+        return a.elapsed_time(b) / len(fns)
+
+    def flushed(self, fn, steps):
+        """L2 flushed before each call; each call between its own events."""
+        torch = self.torch
+        if self.scratch is None:
+            self.scratch = torch.empty(256 * MiB, dtype=torch.uint8, device=self.dev)
+        for _ in range(self.warmup):
+            fn()
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+        with torch.cuda.stream(self.s):
+            for a, b in evs:
+                self.scratch.zero_()
+                a.record(self.s)
+                fn()
+                b.record(self.s)
+        self.s.synchronize()
+        return statistics.mean(a.elapsed_time(b) for a, b in evs)
+
+    def host_call(self, direction, src, n, final, rk, dst, steps):
+        """paes_cuda_chunk on host pointers, synchronous; returns (GB/s of input, out_len)."""
+        C, L = self.C, self.L
+        olen = C.c_uint64()
+
+        def call():
+            rc = L.paes_cuda_chunk(direction, src, n, int(final), rk, dst, C.byref(olen), 1)
+            if rc:
+                raise RuntimeError(self.Nt.last_error())
+
+        call()
+        t = time.perf_counter()
+        for _ in range(steps):
+            call()
+        return n * steps / (time.perf_counter() - t) / 1e9, olen.value
+
+    def rotation(self, nbytes_per_step):
+        return max(1, min(64, -(-4 * L2_BYTES // max(nbytes_per_step, 1))))
+
+    # -- config 1: 64 MiB encrypt + decrypt round trip
+    def cfg1(self):
+        torch, paes = self.torch, self.paes
+        d = self.dig["cfg1"]
+        n = d["len"]
+        key = paes.sweep(0, 16)
+        rk = paes.round_keys(key)
+        host = self.pinned(n + 16)
+        paes.sweep_into(0, n, host.data_ptr())
+        R = self.rotation(2 * n)
+        src = [host[:n].to(self.dev) for _ in range(R)]
+        ct = [torch.empty(n + 16, dtype=torch.uint8, device=self.dev) for _ in range(R)]
+        back = [torch.empty(n + 16, dtype=torch.uint8, device=self.dev) for _ in range(R)]
+        res = torch.zeros(self.steps + self.warmup, dtype=torch.int64, device=self.dev)
+        assert paes.chunk_device(0, src[0].data_ptr(), n, True, rk, ct[0].data_ptr(), self.dev, self.sp) == n + 16
+        self.s.synchronize()
+        ok = self.sha_dev(ct[0], n + 16) == d["ct_sha256"]
+        raw = torch.empty(n, dtype=torch.uint8, device=self.dev)
+        paes.ecb_device(0, src[0].data_ptr(), raw.data_ptr(), n, rk, self.dev, self.sp)
+        self.s.synchronize()
+        ok_raw = self.sha_dev(raw, n) == d["raw_ecb_sha256"]
+        del raw
+        K = self.steps + self.warmup
+        enc = [lambda i=i: paes.chunk_device(0, src[i % R].data_ptr(), n, True, rk, ct[i % R].data_ptr(), self.dev,
+                                             self.sp) for i in range(K)]
+        for i in range(R):
+            enc[i]()
+        ms = self.queued(enc)
+        dec = [lambda i=i: paes.chunk_device_async(1, ct[i % R].data_ptr(), n + 16, True, rk, back[i % R].data_ptr(),
+                                                   res.data_ptr() + 8 * i, self.dev, self.sp) for i in range(K)]
+        msd = self.queued(dec)
+        dec_ok = set(res.tolist()) == {n} and all(
+            paes.count_mismatch_device(back[i].data_ptr(), src[i].data_ptr(), n, self.dev, self.sp) == 0
+            for i in range(R))
+        sync = [lambda i=i: paes.chunk_device(1, ct[i % R].data_ptr(), n + 16, True, rk, back[i % R].data_ptr(),
+                                              self.dev, self.sp) for i in range(K)]
+        ms_sync = self.queued(sync)
+        del src, ct, back
+        hout = self.pinned(n + 16)
+        e2e_enc, olen = self.host_call(0, host.data_ptr(), n, True, rk, hout.data_ptr(), self.steps)
+        ok_e2e = olen == n + 16 and hashlib.sha256(hout[:olen].numpy()).hexdigest() == d["ct_sha256"]
+        hback = self.pinned(n + 16)
+        e2e_dec, olen_d = self.host_call(1, hout.data_ptr(), n + 16, True, rk, hback.data_ptr(), self.steps)
+        ok_e2e = ok_e2e and olen_d == n and bool(torch.equal(hback[:n], host[:n]))
+        gbs, dgbs = n / ms / 1e6, (n + 16) / msd / 1e6
+        return {"workload": "config1: sweep(0, 64 MiB), key sweep(0,16); always-pad encrypt, final decrypt round trip",
+                "value": round(gbs, 2), "unit": "GB/s", "ms_per_step": round(ms, 4), "pipe_frac": self.pipe_frac(gbs),
+                "l2": f"{R} rotating buffer pairs ({R * 2 * n >> 20} MiB working set)",
+                "decrypt": {"value": round(dgbs, 2), "pipe_frac": self.pipe_frac(dgbs),
+                            "api": "paes_cuda_chunk_device_async (queued; verdict in a device word)",
+                            "sync_api_value": round((n + 16) / ms_sync / 1e6, 2)},
+                "e2e": {"value": round(e2e_enc, 2), "unit": "GB/s", "h2d_bytes_per_step": n, "d2h_bytes_per_step": n + 16,
+                        "decrypt_value": round(e2e_dec, 2), "api": "paes_cuda_chunk (pinned host pointers)"},
+                "parity": "ok" if (ok and ok_raw and dec_ok and ok_e2e) else
+                f"MISMATCH (ct {ok}, raw ecb {ok_raw}, round trip {dec_ok}, e2e {ok_e2e})"}
+
+    # -- config 2: decrypt of the reference's 1 GiB ciphertext
+    def cfg2(self):
+        torch, paes = self.torch, self.paes
+        d = self.dig["cfg2"]
+        n = d["pt_len"]
+        m = (n // 16 + 1) * 16
+        key = paes.sweep(1, 16)
+        rk = paes.round_keys(key)
+        hpt = self.pinned(m)
+        paes.sweep_into(1, n, hpt.data_ptr())
+        pt = hpt[:n].to(self.dev)
+        ct = torch.empty(m, dtype=torch.uint8, device=self.dev)
+        out = torch.empty(m, dtype=torch.uint8, device=self.dev)
+        res = torch.zeros(self.steps + self.warmup, dtype=torch.int64, device=self.dev)
+        paes.chunk_device(0, pt.data_ptr(), n, True, rk, ct.data_ptr(), self.dev, self.sp)
+        self.s.synchronize()
+        ok = self.sha_dev(ct, m) == d["ct_sha256"]
+        K = self.steps + self.warmup
+        dec = [lambda i=i: paes.chunk_device_async(1, ct.data_ptr(), m, True, rk, out.data_ptr(),
+                                                   res.data_ptr() + 8 * i, self.dev, self.sp) for i in range(K)]
+        ms = self.queued(dec)
+        dec_ok = set(res.tolist()) == {n} and paes.count_mismatch_device(out.data_ptr(), pt.data_ptr(), n - n % 16,
+                                                                          self.dev, self.sp) == 0
+        dec_ok = dec_ok and bool(torch.equal(out[n - n % 16:n], pt[n - n % 16:n]))
+        ms_sync = self.queued([lambda: paes.chunk_device(1, ct.data_ptr(), m, True, rk, out.data_ptr(), self.dev,
+                                                         self.sp)] * K)
+        hct = self.pinned(m)
+        hct[:m].copy_(ct)
+        del pt, ct, out
+        hout = self.pinned(m)
+        e2e, olen = self.host_call(1, hct.data_ptr(), m, True, rk, hout.data_ptr(), self.steps)
+        ok_e2e = olen == n and hashlib.sha256(hout[:n].numpy()).hexdigest() == d["pt_sha256"]
+        gbs = m / ms / 1e6
+        return {"workload": "config2: final decrypt of the reference's 1 GiB ciphertext of sweep(1, 1 GiB - 16), "
+                            "key sweep(1,16)",
+                "value": round(gbs, 2), "unit": "GB/s", "ms_per_step": round(ms, 4), "pipe_frac": self.pipe_frac(gbs),
+                "api": "paes_cuda_chunk_device_async (queued; verdict in a device word)",
+                "sync_api_value": round(m / ms_sync / 1e6, 2), "l2": "1 GiB input >> L2",
+                "e2e": {"value": round(e2e, 2), "unit": "GB/s", "h2d_bytes_per_step": m, "d2h_bytes_per_step": n,
+                        "api": "paes_cuda_chunk (pinned host pointers)"},
+                "parity": "ok" if (ok and dec_ok and ok_e2e) else
+                f"MISMATCH (ct {ok}, device decrypt {dec_ok}, e2e {ok_e2e})"}
+
+    # -- config 3: size sweep with a 7-byte tail
+    def cfg3(self):
+        torch, paes = self.torch, self.paes
+        key = paes.sweep(2, 16)
+        rk = paes.round_keys(key)
+        rows, all_ok = [], True
+        self.big = None
+        for e in sorted(self.dig["cfg3"]["sizes"], key=lambda e: e["S"]):
+            S, n, m = e["S"], e["len"], e["ct_len"]
+            host = self.pinned(m)
+            paes.sweep_into(2, n, host.data_ptr())
+            src0 = host[:n].to(self.dev)
+            ct0 = torch.empty(m, dtype=torch.uint8, device=self.dev)
+            paes.chunk_device(0, src0.data_ptr(), n, True, rk, ct0.data_ptr(), self.dev, self.sp)
+            self.s.synchronize()
+            ok = self.sha_dev(ct0, m) == e["ct_sha256"]
+            row = {"S": S, "bytes": n}
+            if 2 * n >= 4 * L2_BYTES or S >= 64 * MiB:
+                R = self.rotation(2 * n)
+                src = [src0] + [src0.clone() for _ in range(R - 1)]
+                ct = [ct0] + [torch.empty(m, dtype=torch.uint8, device=self.dev) for _ in range(R - 1)]
+                K = self.steps + self.warmup
+                ms = self.queued([lambda i=i: paes.chunk_device(0, src[i % R].data_ptr(), n, True, rk,
+                                                                ct[i % R].data_ptr(), self.dev, self.sp)
+                                  for i in range(K)])
+                row["l2"] = f"{R} rotating buffer pair(s), queued"
+                del src, ct
+            else:
+                steps = max(self.steps, 50)
+                ms = self.flushed(lambda: paes.chunk_device(0, src0.data_ptr(), n, True, rk, ct0.data_ptr(), self.dev,
+                                                            self.sp), steps)
+                row["l2"] = "flushed before each call (256 MiB memset), per-call events"
+            gbs = n / ms / 1e6
+            row.update(device_gbs=round(gbs, 3), us_per_call=round(ms * 1e3, 2), pipe_frac=self.pipe_frac(gbs))
+            hout = self.pinned(m)
+            e_steps = self.steps if S >= 16 * MiB else max(self.steps, 200 if S <= MiB else 50)
+            e2e, olen = self.host_call(0, host.data_ptr(), n, True, rk, hout.data_ptr(), e_steps)
+            ok_e2e = olen == m and hashlib.sha256(hout[:m].numpy()).hexdigest() == e["ct_sha256"]
+            row.update(e2e_gbs=round(e2e, 3), parity="ok" if ok and ok_e2e else f"MISMATCH (device {ok}, e2e {ok_e2e})")
+            all_ok = all_ok and ok and ok_e2e
+            rows.append(row)
+            if S == 4 * GiB:
+                self.big = (host, e)  # the pageable / file legs reuse the 4 GiB input
+            del src0, ct0, hout
+            torch.cuda.empty_cache()
+        return {"workload": "config3: sweep(2, S+7) for S = 1 KiB .. 4 GiB, key sweep(2,16), always-pad (nine 0x09)",
+                "unit": "GB/s", "rows": rows, "parity": "ok" if all_ok else "MISMATCH"}
+
+    # -- config 5: 4096 messages, per-message keys, one fused launch
+    def cfg5(self):
+        torch, paes = self.torch, self.paes
+        d = self.dig["cfg5"]
+        nmsg = d["n"]
+        lens = paes.batch_lengths(4, nmsg)
+        in_off, out_off, oi, oo = [], [], 0, 0
+        for L in lens:
+            in_off.append(oi)
+            out_off.append(oo)
+            oi += L
+            oo += L + 16
+        host = self.pinned(oi)
+        rks = bytearray()
+        for i in range(nmsg):
+            seed = (4 << 32) + i
+            paes.sweep_into(seed, lens[i], host.data_ptr() + in_off[i])
+            rks += paes.round_keys(paes.sweep(seed, 16))
+        rks = bytes(rks)
+        src = host[:oi].to(self.dev)
+        dst = torch.empty(oo, dtype=torch.uint8, device=self.dev)
+        back = torch.empty(oo, dtype=torch.uint8, device=self.dev)
+        enc_plan = paes.BatchPlan(0, in_off, out_off, lens, rks, True, self.dev)
+        clen = [L + 16 for L in lens]
+        dec_plan = paes.BatchPlan(1, out_off, out_off, clen, rks, True, self.dev)
+        try:
+            enc_plan.run(src.data_ptr(), dst.data_ptr(), self.sp)
+            self.s.synchronize()
+            hct = self.pinned(oo)
+            hct[:oo].copy_(dst)
+            ok = hashlib.sha256(hct[:oo].numpy()).hexdigest() == d["ct_concat_sha256"]
+            K = self.steps + self.warmup
+            ms = self.queued([lambda: enc_plan.run(src.data_ptr(), dst.data_ptr(), self.sp)] * K)
+            msd = self.queued([lambda: dec_plan.run(dst.data_ptr(), back.data_ptr(), self.sp)] * K)
+            dec_ok = dec_plan.run(dst.data_ptr(), back.data_ptr(), self.sp) == lens
+            ms1 = self.queued([lambda: paes.ecb_batch(0, src.data_ptr(), dst.data_ptr(), in_off, out_off, lens, rks,
+                                                      True, self.dev, self.sp)] * K)
+        finally:
+            enc_plan.close()
+            dec_plan.close()
+        del src, dst, back
+        hout = self.pinned(oo)
+        paes.ecb_batch_host(0, host.data_ptr(), hout.data_ptr(), in_off, out_off, lens, rks, True, self.dev)
+        ok_e2e = bool(torch.equal(hout[:oo], hct[:oo]))
+        t = time.perf_counter()
+        for _ in range(self.steps):
+            paes.ecb_batch_host(0, host.data_ptr(), hout.data_ptr(), in_off, out_off, lens, rks, True, self.dev)
+        e2e = oi * self.steps / (time.perf_counter() - t) / 1e9
+        gbs, dgbs = oi / ms / 1e6, oo / msd / 1e6
+        return {"workload": "config5: 4096 msgs, log-uniform 4 KiB..4 MiB, keys sweep((4<<32)+i,16), one fused launch",
+                "value": round(gbs, 2), "unit": "GB/s", "total_bytes": oi, "ms_per_step": round(ms, 4),
+                "pipe_frac": self.pipe_frac(gbs), "api": "paes_cuda_batch_plan_run (prepared plan, one launch)",
+                "one_shot_api_value": round(oi / ms1 / 1e6, 2), "l2": f"{oi >> 20} MiB input >> L2",
+                "decrypt": {"value": round(dgbs, 2), "pipe_frac": self.pipe_frac(dgbs)},
+                "e2e": {"value": round(e2e, 2), "unit": "GB/s", "h2d_bytes_per_step": oi, "d2h_bytes_per_step": oo,
+                        "api": "paes_cuda_batch_host (pinned host; message groups pipelined over 3 streams)"},
+                "parity": "ok" if (ok and dec_ok and ok_e2e) else
+                f"MISMATCH (ct {ok}, round trip {dec_ok}, e2e {ok_e2e})"}
+
+    # -- pageable e2e: the drop-in call on ordinary Python bytes
+    def pageable(self):
+        paes = self.paes
+        host, e = self.big
+        n, m = e["len"], e["ct_len"]
+        data = host[:n].numpy().tobytes()  # ordinary (pageable) bytes, as a _paes caller passes them
+        steps = max(3, min(self.steps, 5))
+        key = paes.sweep(2, 16)
+        out = paes.encrypt_bytes(data, key)
+        ok = len(out) == m and hashlib.sha256(out).hexdigest() == e["ct_sha256"]
+        t = time.perf_counter()
+        for _ in range(steps):
+            out = paes.encrypt_bytes(data, key)
+        enc = n * steps / (time.perf_counter() - t) / 1e9
+        t = time.perf_counter()
+        for _ in range(steps):
+            back = paes.decrypt_bytes(out, key)
+        dec = m * steps / (time.perf_counter() - t) / 1e9
+        ok = ok and back == data
+        return {"workload": "config3's 4 GiB + 7 input as Python bytes (pageable host memory)",
+                "value": round(enc, 2), "unit": "GB/s", "decrypt_value": round(dec, 2),
+                "h2d_bytes_per_step": n, "d2h_bytes_per_step": m,
+                "api": "paes.encrypt_bytes / decrypt_bytes (the _paes drop-in; library-staged pinned ring)",
+                "parity": "ok" if ok else "MISMATCH"}
+
+    # -- the paper's own metric: file -> file run_job, next to the reference's
+    def file_e2e(self):
+        import oracle
+
+        paes = self.paes
+        host, e = self.big
+        n, m = e["len"], e["ct_len"]
+        d = "/dev/shm" if os.path.isdir("/dev/shm") else tempfile.gettempdir()
+        free = shutil.disk_usage(d).free
+        if free < 3 * m + 64 * MiB:
+            return {"skipped": f"{d} has {free} B free, needs {3 * m + 64 * MiB}"}
+        src, ct, pt = (os.path.join(d, f"paes_bench_{x}_{os.getpid()}.bin") for x in ("in", "ct", "pt"))
+        try:
+            host[:n].numpy().tofile(src)
+            key = paes.sweep(2, 16)
+            R = oracle.RefLib()
+            phys, logical = R.cores()
+
+            def cell(fn):
+                fn()  # warm: page cache, CUDA context, pinned ring
+                samples = [fn() for _ in range(3)]
+                kept = R.reject_outliers(samples)  # measure_cell (bench.cpp:81-107)
+                return sum(kept) / len(kept), samples
+
+            enc_s, enc_samples = cell(lambda: paes.encrypt_file(src, ct, key, workers=1, strategy="gpu")["seconds"])
+            ok = hashlib.sha256(open(ct, "rb").read()).hexdigest() == e["ct_sha256"]
+            dec_s, _ = cell(lambda: paes.decrypt_file(ct, pt, key, workers=1, strategy="gpu")["seconds"])
+            ok = ok and hashlib.sha256(open(pt, "rb").read()).hexdigest() == e["pt_sha256"]
+            os.unlink(pt)
+
+            def ref_job():
+                rc, _, _, sec = R.run_job(src, pt, key, logical, 1, 0)
+                assert rc == 0, rc
+                return sec
+
+            ref_s, ref_samples = cell(ref_job)
+            ok = ok and open(pt, "rb").read() == open(ct, "rb").read()
+            return {"workload": f"run_job encrypt/decrypt file -> file on {d}, config3's 4 GiB + 7 input "
+                                f"(JobOutcome.seconds, measure_cell: 1 warm + 3 reps, reject_outliers mean)",
+                    "value": round(n / enc_s / 1e9, 3), "unit": "GB/s", "mbps": round(n * 8 / enc_s / 1e6, 1),
+                    "decrypt_value": round(m / dec_s / 1e9, 3),
+                    "api": "paes_cuda_run_job (strategy gpu: pread -> pinned ring -> GPU -> writer, temp + rename)",
+                    "seconds": [round(x, 4) for x in enc_samples],
+                    "cpu_baseline": {"value": round(n / ref_s / 1e9, 3), "unit": "GB/s", "cores": logical,
+                                     "physical_cores": phys, "kind": "reference",
+                                     "sample": f"reference run_job(threads, {logical} workers) on the same file",
+                                     "seconds": [round(x, 4) for x in ref_samples]},
+                    "parity": "ok (sha256 == reference digest; reference output identical)" if ok else "MISMATCH"}
+        finally:
+            for p in (src, ct, pt):
+                if os.path.exists(p):
+                    os.unlink(p)
+
+
+def run_configs(args, torch, paes, dev, sms):
+    cb = ConfigBench(args, torch, paes, dev, sms)
+    out = {}
+    peaks, _ = measured_peaks()
+    t0 = time.perf_counter()
+    with ClockSampler(dev) as clk:
+        for name, fn in [("config1", cb.cfg1), ("config2", cb.cfg2), ("config3", cb.cfg3), ("config5", cb.cfg5)]:
+            try:
+                out[name] = fn()
+            except Exception as e:  # one config's failure must not lose the headline line
+                out[name] = {"error": f"{type(e).__name__}: {e}"}
+            torch.cuda.empty_cache()
+    cb.clk_mhz = None
+    clocks = clk.summary(peaks.get("sm_max_mhz", 1965.0))
+    # pipe fractions at the clock sampled over the config runs
+    if clocks.get("sm_mhz"):
+        scale = 1965.0 / clocks["sm_mhz"]
+        for v in out.values():
+            for row in [v] + [v.get("decrypt") or {}] + list(v.get("rows") or []):
+                if isinstance(row, dict) and "pipe_frac" in row:
+                    row["pipe_frac"] = round(row["pipe_frac"] * scale, 4)
+    out["clocks"] = clocks
+    for name, fn in [("e2e_pageable", cb.pageable), ("file_e2e", cb.file_e2e)]:
+        try:
+            out[name] = fn() if cb.big is not None else {"skipped": "config 3's 4 GiB input unavailable"}
+        except Exception as e:
+            out[name] = {"error": f"{type(e).__name__}: {e}"}
+    out["seconds"] = round(time.perf_counter() - t0, 1)
+    return out
 
 
 def main():
@@ -545,6 +1008,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-decrypt", action="store_true")
+    ap.add_argument("--no-configs", action="store_true", help="skip configs 1/2/3/5 + pageable/file legs")
     ap.add_argument("--ref-step-s", type=float, default=3.0, help="seconds of CPU work per reference step")
     args = ap.parse_args()
     if args.warmup < 3 and os.environ.get("PAES_BENCH_ALLOW_SHORT") != "1":
@@ -574,8 +1038,11 @@ def main():
     dist = Dist(args.gpus, backend="gloo" if shared else "nccl")
     try:
         res = run_b200(args, dist)
-        if res is not None and dist.rank == 0 and dist.world == 1 and not args.no_cpu:
+        if res is not None and dist.rank == 0 and not args.no_cpu:
+            # rank 0 only, after every rank's timed regions (the other ranks
+            # wait in the final barrier, idle)
             res["cpu_baseline"] = cpu_baseline(args)
+        dist.barrier()
         if res is not None and dist.rank == 0:
             print(json.dumps(res), flush=True)
     finally:

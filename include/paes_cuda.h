@@ -130,7 +130,9 @@ int paes_cuda_sbox(int inverse, uint8_t out[256]);
 int paes_cuda_ecb(int dir, const uint8_t* in, uint8_t* out, uint64_t len, const uint8_t rk[176], int ngpus);
 
 /* Same transform on device-resident buffers of `device`, enqueued on `stream`
- * (a cudaStream_t; NULL = legacy default stream).  Asynchronous. */
+ * (a cudaStream_t; NULL = legacy default stream).  Asynchronous.  Like every
+ * entry point here, in and out must be the same buffer or disjoint: a partial
+ * overlap is PAES_EINVAL (aes.hpp:84-85 allows exact aliasing only). */
 int paes_cuda_ecb_device(int dir, const void* d_in, void* d_out, uint64_t len, const uint8_t rk[176], int device,
                          void* stream);
 
@@ -151,6 +153,21 @@ int paes_cuda_chunk(int dir, const uint8_t* in, uint64_t len, int is_final, cons
  * a length, chunk.cpp:90-100). */
 int paes_cuda_chunk_device(int dir, const void* d_in, uint64_t len, int is_final, const uint8_t rk[176], void* d_out,
                            uint64_t* out_len, int device, void* stream);
+
+/* Queued form of paes_cuda_chunk_device: never synchronises, so a final
+ * decrypt can sit in a stream or a CUDA graph next to other work (the
+ * reference's decrypt_chunk_into checks the trailer before it returns a
+ * length, exec.cpp:122-127 / chunk.cpp:90-100; here the check runs in the
+ * kernel and its verdict is written to device memory).  When the kernel has
+ * run, *d_result -- an 8-byte aligned word in device memory or mapped pinned
+ * host memory -- holds the output length (the unpadded length for a final
+ * decrypt), or PAES_BAD_PAD when the trailer is malformed (the PaddingError
+ * of the synchronous call).  Argument errors are reported at the call
+ * (PAES_EINVAL, or PAES_EBADMSG for a zero-length final decrypt, as
+ * unpad_final raises it before reading any data). */
+#define PAES_BAD_PAD UINT64_MAX
+int paes_cuda_chunk_device_async(int dir, const void* d_in, uint64_t len, int is_final, const uint8_t rk[176],
+                                 void* d_out, uint64_t* d_result, int device, void* stream);
 
 /* ---- multi-key batch (config 5) -----------------------------------------
  * n independent messages, message i = d_in[in_off[i] .. +lens[i]) under the

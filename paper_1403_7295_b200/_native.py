@@ -61,6 +61,7 @@ SIGNATURES = [
     ("paes_cuda_ecb_device", C.c_int, [C.c_int, _vp, _vp, _u64, _vp, C.c_int, _vp]),
     ("paes_cuda_chunk", C.c_int, [C.c_int, _vp, _u64, C.c_int, _vp, _vp, C.POINTER(_u64), C.c_int]),
     ("paes_cuda_chunk_device", C.c_int, [C.c_int, _vp, _u64, C.c_int, _vp, _vp, C.POINTER(_u64), C.c_int, _vp]),
+    ("paes_cuda_chunk_device_async", C.c_int, [C.c_int, _vp, _u64, C.c_int, _vp, _vp, _vp, C.c_int, _vp]),
     ("paes_cuda_ecb_batch", C.c_int, [C.c_int, _vp, _vp, C.POINTER(_u64), C.POINTER(_u64), C.POINTER(_u64), _vp,
                                       C.c_uint32, C.c_int, C.POINTER(_u64), C.c_int, _vp]),
     ("paes_cuda_batch_host", C.c_int, [C.c_int, _vp, _vp, C.POINTER(_u64), C.POINTER(_u64), C.POINTER(_u64), _vp,

@@ -16,7 +16,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB_DIR = os.path.join(PKG, "lib")
 LIB = os.path.join(LIB_DIR, "libpaes_cuda.so")
-SOURCES = ["aes_kernels.cu", "aes_bitsliced.cu", "runtime.cu", "abi_core.cu", "abi_batch.cu", "abi_file.cu", "host_rules.cpp"]
+SOURCES = ["aes_kernels.cu", "runtime.cu", "abi_core.cu", "abi_batch.cu", "abi_file.cu", "host_rules.cpp"]
 HEADERS = ["aes_kernels.cuh", "aes_tables.hpp", "host_rules.hpp", "launch.hpp", "runtime.hpp", "sbox_bitsliced.inc",
            "gpu_worker.cpp"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
@@ -73,7 +73,25 @@ def build(force: bool = False, verbose: bool = False, defines=(), out_lib: str |
         os.unlink(o)
     if out_lib is None:
         build_worker()
+        build_bitsliced_ab()
     return lib
+
+
+BITSLICED_AB = os.path.join(LIB_DIR, "libpaes_bitsliced_ab.so")
+
+
+def build_bitsliced_ab() -> str:
+    """The bitsliced (LOP3) encrypt kernel of the north_star T-table vs
+    bitsliced A/B, in a library of its own so the product .so carries only the
+    shipped kernels (csrc/aes_bitsliced.cu + the host key rules)."""
+    tmp = BITSLICED_AB + ".tmp"
+    cmd = [NVCC] + CCBIN + ARCH + FLAGS + ["-shared", "-o", tmp, os.path.join(CSRC, "aes_bitsliced.cu"),
+                                           os.path.join(CSRC, "host_rules.cpp")]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError("bitsliced A/B build failed:\n%s%s" % (r.stdout, r.stderr))
+    os.replace(tmp, BITSLICED_AB)
+    return BITSLICED_AB
 
 
 WORKER = os.path.join(LIB_DIR, "paes_gpu_worker")

@@ -155,6 +155,7 @@ int paes_cuda_ecb_device(int dir, const void* d_in, void* d_out, uint64_t len, c
     if (!rk) throw std::invalid_argument("null round keys");
     if (len == 0) return PAES_OK;
     if (!d_in || !d_out) throw std::invalid_argument("null device buffer");
+    check_alias(d_in, len, d_out, len);
     DevCtx& d = device(device_id);
     DeviceGuard g(device_id);
     const bool dec = dir == PAES_DECRYPT;
@@ -167,38 +168,62 @@ int paes_cuda_ecb_device(int dir, const void* d_in, void* d_out, uint64_t len, c
   });
 }
 
+}  // extern "C"
+
+namespace {
+
+// Argument rules of encrypt_chunk / decrypt_chunk (exec.cpp:375-392,
+// chunk.cpp:90-100) for the device-pointer entries, checked on the host
+// before any device work; returns the transform's range and output bytes.
+Range device_chunk_range(int dir, const void* d_in, uint64_t len, int is_final, const uint8_t* rk, const void* d_out,
+                         uint64_t* out_bytes) {
+  if (dir != PAES_ENCRYPT && dir != PAES_DECRYPT) throw std::invalid_argument("bad dir");
+  if (!rk) throw std::invalid_argument("null round keys");
+  const bool dec = dir == PAES_DECRYPT;
+  const bool final = is_final != 0;
+  if (!final && len % 16 != 0) throw std::invalid_argument("non-final chunk length must be a multiple of 16");
+  if (dec && len % 16 != 0) throw std::invalid_argument("decrypt: length must be a multiple of 16");
+  if (dec && final && len == 0) throw PaddingError("unpad: length must be a non-zero multiple of 16");
+  Range r;
+  r.dec = dec;
+  r.pad = !dec && final;
+  r.check_pad = dec && final;
+  r.in_len = len;
+  *out_bytes = r.pad ? (len / 16 + 1) * 16 : len;
+  if (*out_bytes && ((len && !d_in) || !d_out)) throw std::invalid_argument("null device buffer");
+  check_alias(d_in, len, d_out, *out_bytes);
+  return r;
+}
+
+}  // namespace
+
+extern "C" {
+
 int paes_cuda_chunk_device(int dir, const void* d_in, uint64_t len, int is_final, const uint8_t rk[176], void* d_out,
                            uint64_t* out_len, int device_id, void* stream) {
   return guarded([&] {
-    if (dir != PAES_ENCRYPT && dir != PAES_DECRYPT) throw std::invalid_argument("bad dir");
-    if (!rk) throw std::invalid_argument("null round keys");
-    const bool dec = dir == PAES_DECRYPT;
-    const bool final = is_final != 0;
-    if (!final && len % 16 != 0) throw std::invalid_argument("non-final chunk length must be a multiple of 16");
-    if (dec && len % 16 != 0) throw std::invalid_argument("decrypt: length must be a multiple of 16");
-    if (dec && final && len == 0) throw PaddingError("unpad: length must be a non-zero multiple of 16");
-    Range r;
-    r.dec = dec;
-    r.pad = !dec && final;
-    r.check_pad = dec && final;
-    if (len == 0 && !r.pad) {
+    uint64_t out_bytes = 0;
+    const Range r = device_chunk_range(dir, d_in, len, is_final, rk, d_out, &out_bytes);
+    if (out_bytes == 0) {
       if (out_len) *out_len = 0;
       return PAES_OK;
     }
-    if ((len && !d_in) || !d_out) throw std::invalid_argument("null device buffer");
     DevCtx& d = device(device_id);
     DeviceGuard g(device_id);
     cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const KeyWords kw = r.dec ? dec_key_words(rk) : enc_key_words(rk);
     if (!r.check_pad) {
       EcbArgs a = make_args(r, static_cast<const std::uint8_t*>(d_in), static_cast<std::uint8_t*>(d_out), len, true,
-                            dec ? dec_key_words(rk) : enc_key_words(rk), nullptr);
-      PAES_CK(launch_ecb(dec, a, d.sm_count, s));
+                            kw, nullptr);
+      PAES_CK(launch_ecb(r.dec, a, d.sm_count, s));
       if (out_len) *out_len = a.nblocks * 16;
       return PAES_OK;
     }
+    // A final decrypt returns the unpadded length, so this entry waits for
+    // its kernel; paes_cuda_chunk_device_async is the queued / graph form.
     StatusSlot slot(d);  // a status word of this call's own: concurrent decrypts do not serialise
-    EcbArgs a = make_args(r, static_cast<const std::uint8_t*>(d_in), static_cast<std::uint8_t*>(d_out), len, true,
-                          dec_key_words(rk), slot.dev());
+    EcbArgs a = make_args(r, static_cast<const std::uint8_t*>(d_in), static_cast<std::uint8_t*>(d_out), len, true, kw,
+                          slot.dev());
     // the trailer check writes the mapped word itself: no memset / D2H copy
     *reinterpret_cast<volatile std::uint32_t*>(slot.host()) = 0xffffffffu;  // sentinel: unchecked => PaddingError
     PAES_CK(launch_ecb(true, a, d.sm_count, s));
@@ -206,6 +231,29 @@ int paes_cuda_chunk_device(int dir, const void* d_in, uint64_t len, int is_final
     const std::uint32_t k = *reinterpret_cast<volatile std::uint32_t*>(slot.host());
     if (k == 0xffffffffu) throw PaddingError("unpad: invalid pad bytes");
     if (out_len) *out_len = len - k;
+    return PAES_OK;
+  });
+}
+
+int paes_cuda_chunk_device_async(int dir, const void* d_in, uint64_t len, int is_final, const uint8_t rk[176],
+                                 void* d_out, uint64_t* d_result, int device_id, void* stream) {
+  return guarded([&] {
+    if (!d_result || reinterpret_cast<std::uintptr_t>(d_result) % 8)
+      throw std::invalid_argument("d_result must be an 8-byte aligned device-visible word");
+    uint64_t out_bytes = 0;
+    const Range r = device_chunk_range(dir, d_in, len, is_final, rk, d_out, &out_bytes);
+    DevCtx& d = device(device_id);
+    DeviceGuard g(device_id);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    auto* res = reinterpret_cast<unsigned long long*>(d_result);
+    if (out_bytes == 0) {  // nothing to transform: the result word still gets its value, in stream order
+      PAES_CK(launch_put_u64(res, 0, s));
+      return PAES_OK;
+    }
+    EcbArgs a = make_args(r, static_cast<const std::uint8_t*>(d_in), static_cast<std::uint8_t*>(d_out), len, true,
+                          r.dec ? dec_key_words(rk) : enc_key_words(rk), nullptr);
+    a.result = res;
+    PAES_CK(launch_ecb(r.dec, a, d.sm_count, s));
     return PAES_OK;
   });
 }
@@ -308,17 +356,3 @@ int paes_cuda_count_mismatch_device(const void* d_a, const void* d_b, uint64_t l
 uint64_t paes_cuda_launch_count(void) { return launch_count(); }
 
 }  // extern "C"
-
-// Experimental, not in include/paes_cuda.h: the bitsliced (LOP3) encrypt
-// kernel for the T-table vs bitsliced A/B (scripts/bitsliced_ab.py).
-extern "C" int paes_cuda_experimental_bitsliced_ecb(const void* d_in, void* d_out, uint64_t len, const uint8_t rk[176],
-                                                    int device_id, void* stream) {
-  return guarded([&] {
-    if (len % (16 * 1024)) throw std::invalid_argument("length must be a multiple of 16 KiB");
-    DevCtx& d = device(device_id);
-    DeviceGuard g(device_id);
-    PAES_CK(launch_ecb_bitsliced_experiment(static_cast<const std::uint8_t*>(d_in), static_cast<std::uint8_t*>(d_out),
-                                            len / 16, enc_key_words(rk), d.sm_count, static_cast<cudaStream_t>(stream)));
-    return PAES_OK;
-  });
-}

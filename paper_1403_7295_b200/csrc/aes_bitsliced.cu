@@ -1,7 +1,9 @@
 // aes_bitsliced.cu -- bitsliced AES-128 ECB encrypt for sm_100a: the ALU
 // (LOP3) alternative the north_star asks to A/B against the T-table kernel.
-// Not on the product path: reached only through the experimental entry
-// paes_cuda_experimental_bitsliced_ecb (scripts/bitsliced_ab.py).
+// Not on the product path and not in libpaes_cuda.so: build.py links it into
+// its own A/B library, lib/libpaes_bitsliced_ab.so, whose only entry point
+// paes_bitsliced_ab_ecb is used by scripts/bitsliced_ab.py and
+// tests/test_gpu_bitsliced.py.
 //
 // Layout: each thread owns 32 blocks of a 1024-block warp tile (lane l takes
 // blocks l, l+32, ..., so every 128-bit load/store is coalesced).  The 32x4
@@ -17,7 +19,7 @@
 #include <cstdint>
 
 #include "aes_kernels.cuh"
-#include "launch.hpp"
+#include "host_rules.hpp"
 
 namespace paes_b200 {
 
@@ -150,22 +152,39 @@ __global__ void __launch_bounds__(kBsThreads) ecb_bitsliced_kernel(const std::ui
 }  // namespace
 
 // Whole 1024-block tiles only (the A/B driver sizes its buffers accordingly).
-cudaError_t launch_ecb_bitsliced_experiment(const std::uint8_t* in, std::uint8_t* out, unsigned long long nblocks,
-                                            const KeyWords& kw, int sm_count, cudaStream_t stream) {
+static cudaError_t launch_bitsliced(const std::uint8_t* in, std::uint8_t* out, unsigned long long nblocks,
+                                    const KeyWords& kw, cudaStream_t stream) {
   if (nblocks % 1024) return cudaErrorInvalidValue;
   BsKeys k{};
   for (int r = 0; r < 11; ++r)
     for (int c = 0; c < 4; ++c)
       for (int b = 0; b < 32; ++b) k.m[r][c][b] = ((kw.w[4 * r + c] >> b) & 1u) ? 0xffffffffu : 0u;
-  int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ecb_bitsliced_kernel, kBsThreads, 0);
+  int dev = 0, sm_count = 0, per_sm = 0;
+  cudaError_t e;
+  if ((e = cudaGetDevice(&dev)) || (e = cudaDeviceGetAttribute(&sm_count, cudaDevAttrMultiProcessorCount, dev)) ||
+      (e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ecb_bitsliced_kernel, kBsThreads, 0)))
+    return e;
   const unsigned long long ntiles = nblocks / 1024;
   unsigned long long grid = (ntiles + kBsThreads / 32 - 1) / (kBsThreads / 32);
   const unsigned long long cap = static_cast<unsigned long long>(sm_count) * (per_sm > 0 ? per_sm : 1);
   if (grid > cap) grid = cap;
-  (void)cudaGetLastError();  // report this launch only
-  ecb_bitsliced_kernel<<<static_cast<unsigned>(grid), kBsThreads, 0, stream>>>(in, out, ntiles, k);
-  return cudaGetLastError();
+  if (grid == 0) return cudaSuccess;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(static_cast<unsigned>(grid));
+  cfg.blockDim = dim3(kBsThreads);
+  cfg.stream = stream;
+  return cudaLaunchKernelEx(&cfg, ecb_bitsliced_kernel, in, out, ntiles, k);
 }
 
 }  // namespace paes_b200
+
+// The A/B library's one entry point (current device; 0 ok, -22 for a length
+// that is not whole 16 KiB tiles, -1002 for a CUDA error).
+extern "C" int paes_bitsliced_ab_ecb(const void* d_in, void* d_out, std::uint64_t len, const std::uint8_t rk[176],
+                                     void* stream) {
+  if (len % (16 * 1024) || !rk) return -22;
+  const cudaError_t e =
+      paes_b200::launch_bitsliced(static_cast<const std::uint8_t*>(d_in), static_cast<std::uint8_t*>(d_out), len / 16,
+                                  paes_b200::enc_key_words(rk), static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? 0 : -1002;
+}

@@ -4,6 +4,7 @@
 
 #include <atomic>
 #include <cstdint>
+#include <utility>
 
 #include "../../include/paes_cuda.h"
 #include "aes_kernels.cuh"
@@ -285,9 +286,11 @@ __global__ void __launch_bounds__(kThreads, 1) ecb_kernel(const __grid_constant_
   const std::uint32_t lane4 = lane * 4;
   constexpr unsigned long long kTile = 32ull * NB;
   const unsigned long long ntiles = (a.nblocks + kTile - 1) / kTile;
-  // tiles of whole input blocks; the tile holding a checked trailer goes to
-  // the ragged loop so the pad check always runs
-  const unsigned long long full_tiles = (a.check_pad ? a.nfull - 1 : a.nfull) / kTile;
+  // tiles of whole input blocks; the tile holding the last block goes to the
+  // ragged loop when the call checks a trailer or reports its result, so the
+  // thread that owns that block always runs the epilogue
+  const bool report = a.check_pad || a.result != nullptr;
+  const unsigned long long full_tiles = ((report && a.nblocks == a.nfull) ? a.nfull - 1 : a.nfull) / kTile;
   const unsigned long long wpc = blockDim.x / 32;
   // tiles interleave across CTAs (tile t -> CTA t mod grid), so a short input
   // spreads over many SMs instead of queueing on one SM's lookup pipe
@@ -362,7 +365,15 @@ __global__ void __launch_bounds__(kThreads, 1) ecb_kernel(const __grid_constant_
       const unsigned long long idx = b0 + 32ull * j;
       if (idx < a.nblocks) {
         store_block<ALIGNED>(a.out + 16ull * idx, s[j]);
-        if (DEC && a.check_pad && idx == a.nblocks - 1) *a.status = pad_check(s[j]);
+        if (idx == a.nblocks - 1) {
+          unsigned long long olen = 16ull * a.nblocks;
+          if (DEC && a.check_pad) {
+            const std::uint32_t k = pad_check(s[j]);
+            if (a.status) *a.status = k;
+            olen = k == 0xffffffffu ? ~0ull : olen - k;
+          }
+          if (a.result) *a.result = olen;
+        }
       }
     }
   }
@@ -583,6 +594,8 @@ __global__ void mismatch_kernel(const uint4* a, const uint4* b, unsigned long lo
   if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(out, static_cast<unsigned long long>(cnt));
 }
 
+__global__ void put_u64_kernel(unsigned long long* p, unsigned long long v) { *p = v; }
+
 template <class KernelT>
 cudaError_t set_smem(KernelT k, int bytes) {
   return cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
@@ -609,47 +622,42 @@ cudaError_t prepare_kernels() {
   return cudaSuccess;
 }
 
-// Launchers report cudaGetLastError() after the launch; a stale non-sticky
-// error left by an earlier, unrelated call (ours or the caller's) is cleared
-// first, so the report covers this launch only.
-static void clear_stale_error() { (void)cudaGetLastError(); }
+// Every launch goes through cudaLaunchKernelEx, whose return value is the
+// launch's own error: the calling thread's last-error state (which may hold a
+// non-sticky error the caller has not consumed yet) is neither read nor
+// cleared here.
+template <class... KArgs, class... Args>
+static cudaError_t launch_k(void (*k)(KArgs...), unsigned long long grid, int block, int smem, cudaStream_t stream,
+                            bool pdl, Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(static_cast<unsigned>(grid));
+  cfg.blockDim = dim3(static_cast<unsigned>(block));
+  cfg.dynamicSmemBytes = static_cast<std::size_t>(smem);
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  if (pdl) {
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+  }
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, k, std::forward<Args>(args)...);
+  if (e == cudaSuccess) g_launches.fetch_add(1, std::memory_order_relaxed);
+  return e;
+}
 
 cudaError_t launch_ecb(bool dec, const EcbArgs& args, int sm_count, cudaStream_t stream) {
   if (args.nblocks == 0) return cudaSuccess;
   // one CTA per SM, or one per warp tile when there are fewer tiles than SMs
   const unsigned long long ntiles = (args.nblocks + 32ull * kNB - 1) / (32ull * kNB);
   const unsigned long long grid = ntiles < static_cast<unsigned long long>(sm_count) ? ntiles : sm_count;
-  clear_stale_error();
   const bool aligned = ((reinterpret_cast<std::uintptr_t>(args.in) | reinterpret_cast<std::uintptr_t>(args.out)) & 15) == 0;
   const int smem = dec ? kDecLaunchSmem : kEncLaunchSmem;
-#if PAES_PDL
-  cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(static_cast<unsigned>(grid));
-  cfg.blockDim = dim3(kThreads);
-  cfg.dynamicSmemBytes = static_cast<std::size_t>(smem);
-  cfg.stream = stream;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  cudaError_t le;
-  if (dec) le = aligned ? cudaLaunchKernelEx(&cfg, ecb_kernel<true, kNB, true>, args)
-                        : cudaLaunchKernelEx(&cfg, ecb_kernel<true, kNB, false>, args);
-  else le = aligned ? cudaLaunchKernelEx(&cfg, ecb_kernel<false, kNB, true>, args)
-                    : cudaLaunchKernelEx(&cfg, ecb_kernel<false, kNB, false>, args);
-  if (le != cudaSuccess) return le;
-#else
-  if (dec) {
-    if (aligned) ecb_kernel<true, kNB, true><<<static_cast<unsigned>(grid), kThreads, smem, stream>>>(args);
-    else ecb_kernel<true, kNB, false><<<static_cast<unsigned>(grid), kThreads, smem, stream>>>(args);
-  } else {
-    if (aligned) ecb_kernel<false, kNB, true><<<static_cast<unsigned>(grid), kThreads, smem, stream>>>(args);
-    else ecb_kernel<false, kNB, false><<<static_cast<unsigned>(grid), kThreads, smem, stream>>>(args);
-  }
-#endif
-  g_launches.fetch_add(1, std::memory_order_relaxed);
-  return cudaGetLastError();
+  const bool pdl = PAES_PDL != 0;
+  if (dec) return aligned ? launch_k(ecb_kernel<true, kNB, true>, grid, kThreads, smem, stream, pdl, args)
+                          : launch_k(ecb_kernel<true, kNB, false>, grid, kThreads, smem, stream, pdl, args);
+  return aligned ? launch_k(ecb_kernel<false, kNB, true>, grid, kThreads, smem, stream, pdl, args)
+                 : launch_k(ecb_kernel<false, kNB, false>, grid, kThreads, smem, stream, pdl, args);
 }
 
 unsigned batch_tile_blocks() { return 32u * kNB; }
@@ -660,56 +668,43 @@ cudaError_t launch_batch(bool dec, const BatchArgs& args, int sm_count, cudaStre
   const unsigned long long grid =
       args.total_tiles < static_cast<unsigned long long>(sm_count) ? args.total_tiles : sm_count;
   const int smem = dec ? kDecLaunchSmem : kEncLaunchSmem;
-  clear_stale_error();
   const bool aligned =
       args.aligned && ((reinterpret_cast<std::uintptr_t>(args.in) | reinterpret_cast<std::uintptr_t>(args.out)) & 15) == 0;
-  const dim3 g(static_cast<unsigned>(grid));
-  if (dec) {
-    if (aligned) batch_kernel<true, kNB, true><<<g, kThreads, smem, stream>>>(args);
-    else batch_kernel<true, kNB, false><<<g, kThreads, smem, stream>>>(args);
-  } else {
-    if (aligned) batch_kernel<false, kNB, true><<<g, kThreads, smem, stream>>>(args);
-    else batch_kernel<false, kNB, false><<<g, kThreads, smem, stream>>>(args);
-  }
-  g_launches.fetch_add(1, std::memory_order_relaxed);
-  return cudaGetLastError();
+  if (dec) return aligned ? launch_k(batch_kernel<true, kNB, true>, grid, kThreads, smem, stream, false, args)
+                          : launch_k(batch_kernel<true, kNB, false>, grid, kThreads, smem, stream, false, args);
+  return aligned ? launch_k(batch_kernel<false, kNB, true>, grid, kThreads, smem, stream, false, args)
+                 : launch_k(batch_kernel<false, kNB, false>, grid, kThreads, smem, stream, false, args);
 }
 
 cudaError_t launch_state_op(int op, std::uint8_t* d_states, unsigned long long n, const StateKey& rk,
                             cudaStream_t stream) {
   if (n == 0) return cudaSuccess;
-  clear_stale_error();
-  state_op_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, stream>>>(op, d_states, n, rk);
-  g_launches.fetch_add(1, std::memory_order_relaxed);
-  return cudaGetLastError();
+  return launch_k(state_op_kernel, (n + 255) / 256, 256, 0, stream, false, op, d_states, n, rk);
 }
 
 cudaError_t launch_counter_fill(unsigned long long seed, unsigned long long word0, unsigned long long nwords, void* out,
                                 int sm_count, cudaStream_t stream) {
   if (nwords == 0) return cudaSuccess;
-  clear_stale_error();
-  counter_fill_kernel<<<sm_count * 4, 512, 0, stream>>>(seed, word0, nwords, static_cast<unsigned long long*>(out));
-  g_launches.fetch_add(1, std::memory_order_relaxed);
-  return cudaGetLastError();
+  return launch_k(counter_fill_kernel, sm_count * 4ull, 512, 0, stream, false, seed, word0, nwords,
+                  static_cast<unsigned long long*>(out));
 }
 
 cudaError_t launch_checksum(const void* buf, unsigned long long nwords, unsigned long long base, unsigned long long* d_out,
                             int sm_count, cudaStream_t stream) {
   if (nwords == 0) return cudaSuccess;
-  clear_stale_error();
-  checksum_kernel<<<sm_count * 4, 512, 0, stream>>>(static_cast<const unsigned long long*>(buf), nwords, base, d_out);
-  g_launches.fetch_add(1, std::memory_order_relaxed);
-  return cudaGetLastError();
+  return launch_k(checksum_kernel, sm_count * 4ull, 512, 0, stream, false,
+                  static_cast<const unsigned long long*>(buf), nwords, base, d_out);
 }
 
 cudaError_t launch_mismatch(const void* a, const void* b, unsigned long long nblocks, unsigned long long* d_out,
                             int sm_count, cudaStream_t stream) {
   if (nblocks == 0) return cudaSuccess;
-  clear_stale_error();
-  mismatch_kernel<<<sm_count * 4, 512, 0, stream>>>(static_cast<const uint4*>(a), static_cast<const uint4*>(b), nblocks,
-                                                   d_out);
-  g_launches.fetch_add(1, std::memory_order_relaxed);
-  return cudaGetLastError();
+  return launch_k(mismatch_kernel, sm_count * 4ull, 512, 0, stream, false, static_cast<const uint4*>(a),
+                  static_cast<const uint4*>(b), nblocks, d_out);
+}
+
+cudaError_t launch_put_u64(unsigned long long* p, unsigned long long v, cudaStream_t stream) {
+  return launch_k(put_u64_kernel, 1, 1, 0, stream, false, p, v);
 }
 
 unsigned long long launch_count() { return g_launches.load(std::memory_order_relaxed); }

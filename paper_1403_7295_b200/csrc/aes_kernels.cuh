@@ -74,7 +74,12 @@ struct EcbArgs {
   unsigned long long nfull;    // blocks read whole from `in` (nblocks or nblocks-1)
   std::uint32_t tail_len;      // bytes at in[16*nfull ..] forming the pad block (0..15)
   std::uint32_t check_pad;     // decrypt: validate PKCS#7 trailer of block nblocks-1
-  std::uint32_t* status;       // decrypt pad result: pad byte k (1..16) or 0xffffffff
+  std::uint32_t* status;       // decrypt pad result: pad byte k (1..16) or 0xffffffff (nullable)
+  // optional device-visible word written by the thread that owns the last
+  // block: the output length (16 * nblocks, minus the pad for a checked
+  // trailer) or ~0 for a malformed trailer -- the asynchronous face of
+  // decrypt_chunk_into's unpad_final (exec.cpp:122-127)
+  unsigned long long* result;
   KeyWords k;
 };
 

@@ -21,13 +21,8 @@ cudaError_t launch_mismatch(const void* a, const void* b, unsigned long long nbl
 // Single-state round transforms (PAES_OP_*) on n device-resident states.
 cudaError_t launch_state_op(int op, std::uint8_t* d_states, unsigned long long n, const StateKey& rk,
                             cudaStream_t stream);
+// One 64-bit store on the stream (a result word for an empty transform).
+cudaError_t launch_put_u64(unsigned long long* p, unsigned long long v, cudaStream_t stream);
 unsigned long long launch_count();
 
-}  // namespace paes_b200
-
-namespace paes_b200 {
-// Experimental bitsliced encrypt (aes_bitsliced.cu): the LOP3 alternative of
-// the north_star A/B.  Whole 1024-block tiles only.
-cudaError_t launch_ecb_bitsliced_experiment(const std::uint8_t* in, std::uint8_t* out, unsigned long long nblocks,
-                                            const KeyWords& kw, int sm_count, cudaStream_t stream);
 }  // namespace paes_b200

@@ -51,13 +51,28 @@ std::uint64_t g_chunk = 256ull << 20;
 int g_streams = 3;
 std::atomic<std::uint64_t> g_zero_copy_max{48ull << 20};  // scripts/ring_piece_sweep.py: the ring wins from ~64 MiB
 
+// The device count is fixed for the life of a process once CUDA has
+// initialised: cached after the first successful query (hot device-pointer
+// calls validate their device index against it on every call).
 int visible_devices() {
+  static std::atomic<int> cached{-1};
+  const int c = cached.load(std::memory_order_relaxed);
+  if (c > 0) return c;
   int n = 0;
   if (cudaGetDeviceCount(&n) != cudaSuccess) {
     cudaGetLastError();
     return 0;
   }
+  if (n > 0) cached.store(n, std::memory_order_relaxed);
   return n;
+}
+
+void check_alias(const void* in, std::uint64_t in_len, const void* out, std::uint64_t out_len) {
+  if (in == out || in_len == 0 || out_len == 0 || !in || !out) return;
+  const std::uintptr_t a = reinterpret_cast<std::uintptr_t>(in), b = reinterpret_cast<std::uintptr_t>(out);
+  if (a < b + out_len && b < a + in_len)
+    throw std::invalid_argument("in and out overlap without being the same buffer (they may only alias exactly, "
+                                "aes.hpp:84-85)");
 }
 
 // CPUs of a device's NUMA node (from sysfs via its PCI address); empty when
@@ -113,8 +128,9 @@ DevCtx& device(int id) {
   if (id < 0 || id >= n || id >= kMaxDev)
     throw CudaFail{PAES_ENODEV, "no such CUDA device: " + std::to_string(id) + " (visible: " + std::to_string(n) + ")"};
   DevCtx& d = g_dev[id];
+  if (d.ready.load(std::memory_order_acquire)) return d;
   std::lock_guard<std::mutex> lk(d.mu);
-  if (!d.ready) {
+  if (!d.ready.load(std::memory_order_relaxed)) {
     DeviceGuard g(id);
     PAES_CK(cudaDeviceGetAttribute(&d.sm_count, cudaDevAttrMultiProcessorCount, id));
     PAES_CK(prepare_kernels());
@@ -128,7 +144,7 @@ DevCtx& device(int id) {
     PAES_CK(cudaMalloc(&d.d_acc, 64));
     PAES_CK(cudaMallocHost(&d.h_acc, 64));
     d.id = id;
-    d.ready = true;
+    d.ready.store(true, std::memory_order_release);
   }
   return d;
 }
@@ -671,6 +687,7 @@ int host_transform(int dir, const std::uint8_t* in, std::uint64_t len, bool is_f
     return PAES_OK;
   }
   if (!out) throw std::invalid_argument("null output");
+  check_alias(in, len, out, (is_final && !dec) ? (len / 16 + 1) * 16 : len);
   const auto devs = device_list(ngpus);
   const KeyWords kw = dec ? dec_key_words(rk) : enc_key_words(rk);
   const auto plan = dec ? plan_decrypt_chunks(len, static_cast<unsigned>(devs.size()))

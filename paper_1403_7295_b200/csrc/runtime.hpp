@@ -6,6 +6,7 @@
 
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <condition_variable>
 #include <cstdint>
 #include <exception>
@@ -107,7 +108,7 @@ class CopyTeam {
 // ------------------------------------------------------------ device context
 struct DevCtx {
   int id = -1;
-  bool ready = false;
+  std::atomic<bool> ready{false};  // set once, after every field below is initialised
   int sm_count = 0;
   std::mutex mu;  // serialises host-pointer pipelines / status words on this device
   std::vector<cudaStream_t> st;
@@ -195,6 +196,12 @@ struct Range {
   bool check_pad = false;  // decrypt: validate the trailer
   std::uint64_t in_len = 0;
 };
+
+// In and out may be the same buffer (aes.hpp:84-85: "may alias exactly") or
+// disjoint; a partial overlap would let one CTA overwrite input another has
+// not read yet, so it is rejected (std::invalid_argument) before any device
+// work.  Host-only: safe to call without a GPU.
+void check_alias(const void* in, std::uint64_t in_len, const void* out, std::uint64_t out_len);
 
 EcbArgs make_args(const Range& r, const std::uint8_t* in, std::uint8_t* out, std::uint64_t in_len, bool last,
                   const KeyWords& kw, std::uint32_t* status);

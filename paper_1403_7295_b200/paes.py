@@ -414,6 +414,19 @@ def chunk_device(direction: int, d_in: int, nbytes: int, is_final: bool, rk: byt
     return olen.value
 
 
+BAD_PAD = (1 << 64) - 1  # PAES_BAD_PAD: the result word of a final decrypt with a malformed trailer
+
+
+def chunk_device_async(direction: int, d_in: int, nbytes: int, is_final: bool, rk: bytes, d_out: int, d_result: int,
+                       device: int = 0, stream: int = 0) -> None:
+    """Queued chunk transform (paes_cuda_chunk_device_async): never syncs, so
+    it can be captured in a CUDA graph.  When it has run, the uint64 at
+    ``d_result`` (device or mapped pinned memory) holds the output length --
+    the unpadded length for a final decrypt -- or ``BAD_PAD``."""
+    _raise(N.load().paes_cuda_chunk_device_async(direction, d_in, nbytes, int(bool(is_final)), _rk176(rk), d_out,
+                                                 d_result, device, stream or None))
+
+
 def _u64_array(xs):
     import numpy as np
 

@@ -15,9 +15,10 @@ from paper_1403_7295_b200 import _native as N  # noqa: E402
 from paper_1403_7295_b200 import paes  # noqa: E402
 
 profile = "--profile" in sys.argv
-L = N.load()
-L.paes_cuda_experimental_bitsliced_ecb.argtypes = [C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p, C.c_int,
-                                                   C.c_void_p]
+from paper_1403_7295_b200 import build as B  # noqa: E402
+
+BS = C.CDLL(B.BITSLICED_AB)
+BS.paes_bitsliced_ab_ecb.argtypes = [C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p, C.c_void_p]
 n = (1 << 30) if profile else (8 << 30)
 rk = paes.round_keys(paes.sweep(3, 16))
 pt = torch.empty(n, dtype=torch.uint8, device="cuda")
@@ -32,8 +33,8 @@ def ttable():
 
 
 def bitsliced():
-    rc = L.paes_cuda_experimental_bitsliced_ecb(pt.data_ptr(), b.data_ptr(), n, rk, 0, s.cuda_stream)
-    assert rc == 0, N.last_error()
+    rc = BS.paes_bitsliced_ab_ecb(pt.data_ptr(), b.data_ptr(), n, rk, s.cuda_stream)
+    assert rc == 0, rc
 
 
 res = {"bytes": n}

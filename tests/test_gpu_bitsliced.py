@@ -11,16 +11,15 @@ pytestmark = pytest.mark.gpu
 def test_bitsliced_matches_oracle(paes, gpu, orc):
     import torch
 
-    from paper_1403_7295_b200 import _native as N
+    from paper_1403_7295_b200 import build as B
 
-    L = N.load()
-    fn = L.paes_cuda_experimental_bitsliced_ecb
-    fn.argtypes = [C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p, C.c_int, C.c_void_p]
+    fn = C.CDLL(B.BITSLICED_AB).paes_bitsliced_ab_ecb
+    fn.argtypes = [C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p, C.c_void_p]
     key = os.urandom(16)
     data = os.urandom(16 * 1024 * 37)
     src = torch.frombuffer(bytearray(data), dtype=torch.uint8).cuda()
     dst = torch.empty_like(src)
-    assert fn(src.data_ptr(), dst.data_ptr(), len(data), paes.round_keys(key), 0, None) == 0
+    assert fn(src.data_ptr(), dst.data_ptr(), len(data), paes.round_keys(key), None) == 0
     torch.cuda.synchronize()
     assert dst.cpu().numpy().tobytes() == orc.ecb(0, data, key, threads=4)
-    assert fn(src.data_ptr(), dst.data_ptr(), 100, paes.round_keys(key), 0, None) == N.EINVAL
+    assert fn(src.data_ptr(), dst.data_ptr(), 100, paes.round_keys(key), None) == -22

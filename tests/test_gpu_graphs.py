@@ -83,3 +83,72 @@ def test_batch_plan_captures_and_replays(paes, gpu, orc):
                 assert out[o:o + len(want)].tobytes() == want, rep
     finally:
         plan.close()
+
+
+def test_final_decrypt_async_captures_and_replays(paes, gpu, orc):
+    """The queued final decrypt (paes_cuda_chunk_device_async) records into a
+    graph with the encrypt before it; each replay re-checks the trailer and
+    writes the unpadded length -- or BAD_PAD under a wrong key -- on the device."""
+    import torch
+
+    rnd = random.Random(11)
+    key = rnd.randbytes(16)
+    rk, bad = paes.round_keys(key), paes.round_keys(bytes(16))
+    n = 2 * 1024 * 1024 + 9
+    m = (n // 16 + 1) * 16
+    src = torch.zeros(n + 64, dtype=torch.uint8, device="cuda")
+    ct = torch.zeros(m + 64, dtype=torch.uint8, device="cuda")
+    pt = torch.zeros(m + 64, dtype=torch.uint8, device="cuda")
+    res = torch.zeros(3, dtype=torch.int64, device="cuda")
+    s = torch.cuda.Stream()
+    base = paes.launch_count()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(s):
+        paes.chunk_device_async(paes.ENCRYPT, src.data_ptr(), n, True, rk, ct.data_ptr(), res.data_ptr(), 0,
+                                s.cuda_stream)
+        s.synchronize()
+        with torch.cuda.graph(g, stream=s):
+            paes.chunk_device_async(paes.ENCRYPT, src.data_ptr(), n, True, rk, ct.data_ptr(), res.data_ptr(), 0,
+                                    s.cuda_stream)
+            paes.chunk_device_async(paes.DECRYPT, ct.data_ptr(), m, True, rk, pt.data_ptr(), res.data_ptr() + 8, 0,
+                                    s.cuda_stream)
+            paes.chunk_device_async(paes.DECRYPT, ct.data_ptr(), m, True, bad, pt.data_ptr() + 0, res.data_ptr() + 16,
+                                    0, s.cuda_stream)
+    assert paes.launch_count() - base == 4
+    for rep in range(3):
+        data = rnd.randbytes(n)
+        src[:n].copy_(torch.frombuffer(bytearray(data), dtype=torch.uint8))
+        res.fill_(-2)
+        torch.cuda.synchronize()
+        g.replay()
+        torch.cuda.synchronize()
+        got = [int(x) & ((1 << 64) - 1) for x in res.cpu().tolist()]
+        assert got[0] == m and got[1] == n, (rep, got)
+        want_ct = orc.encrypt_chunk(data, True, key)
+        assert ct[:m].cpu().numpy().tobytes() == want_ct, rep
+        # the wrong key's verdict is whatever unpad_final says of its last block
+        u = orc.unpad(orc.ecb(1, want_ct[-16:], bytes(16)))  # unpadded length of the last block, or < 0
+        assert got[2] == (paes.BAD_PAD if u < 0 else m - 16 + u), (rep, got, u)
+
+
+def test_async_result_word_in_mapped_memory_and_empty_inputs(paes, gpu):
+    """d_result may be mapped pinned host memory; empty transforms still write
+    their result (0) in stream order, and a final encrypt of 0 bytes writes the
+    full pad block (16)."""
+    import torch
+
+    rk = paes.round_keys(bytes(range(16)))
+    host = torch.full((4,), -2, dtype=torch.int64).pin_memory()
+    # torch's pinned blocks are cudaHostAlloc'ed: mapped at the same address under UVA
+    ct = torch.zeros(64, dtype=torch.uint8, device="cuda")
+    s = torch.cuda.Stream()
+    hp = host.data_ptr()
+    paes.chunk_device_async(paes.ENCRYPT, ct.data_ptr(), 0, True, rk, ct.data_ptr(), hp, 0, s.cuda_stream)
+    paes.chunk_device_async(paes.ENCRYPT, ct.data_ptr(), 0, False, rk, ct.data_ptr(), hp + 8, 0, s.cuda_stream)
+    paes.chunk_device_async(paes.DECRYPT, ct.data_ptr(), 16, True, rk, ct.data_ptr() + 16, hp + 16, 0, s.cuda_stream)
+    s.synchronize()
+    assert host.tolist()[:3] == [16, 0, 0]  # E(16 x 0x10) decrypts back to an all-pad block: unpadded length 0
+    with pytest.raises(paes.PaddingError):
+        paes.chunk_device_async(paes.DECRYPT, ct.data_ptr(), 0, True, rk, ct.data_ptr(), hp, 0, s.cuda_stream)
+    with pytest.raises(ValueError):
+        paes.chunk_device_async(paes.ENCRYPT, ct.data_ptr(), 16, True, rk, ct.data_ptr(), hp + 4, 0, s.cuda_stream)

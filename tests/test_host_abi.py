@@ -277,3 +277,32 @@ def test_python_wrappers_check_what_the_abi_cannot(paes):
         paes.ecb_device(0, 1, 1, 16, bytes(16))
     with pytest.raises(ValueError, match="176-byte"):
         paes.chunk_device(0, 1, 16, True, rk + b"x", 1)
+
+
+def test_partial_overlap_is_rejected_before_any_device_work(lib):
+    """in/out may alias exactly (aes.hpp:84-85) or be disjoint; a partial
+    overlap is PAES_EINVAL, decided on the host (this runs without a GPU)."""
+    from paper_1403_7295_b200 import _native as N
+
+    rk = (C.c_uint8 * 176)()
+    buf = (C.c_uint8 * 4096)()
+    base = C.addressof(buf)
+    olen = C.c_uint64()
+    res = (C.c_uint64 * 1)()
+    # device-pointer entries: the check precedes the device lookup
+    assert lib.paes_cuda_ecb_device(0, base, base + 16, 256, rk, 0, None) == N.EINVAL
+    assert "alias" in N.last_error()
+    assert lib.paes_cuda_ecb_device(1, base + 32, base, 256, rk, 0, None) == N.EINVAL
+    assert lib.paes_cuda_chunk_device(0, base, 100, 1, rk, base + 48, C.byref(olen), 0, None) == N.EINVAL
+    # out is the padded length (112 B here), so an input starting at out + 104 overlaps it
+    assert lib.paes_cuda_chunk_device(0, base + 104, 100, 1, rk, base, C.byref(olen), 0, None) == N.EINVAL
+    assert lib.paes_cuda_chunk_device_async(1, base, 256, 1, rk, base + 128, res, 0, None) == N.EINVAL
+    # host-pointer entries
+    assert lib.paes_cuda_ecb(0, buf, C.cast(base + 16, C.POINTER(C.c_uint8)), 256, rk, 0) == N.EINVAL
+    assert lib.paes_cuda_chunk(0, buf, 100, 1, rk, C.cast(base + 64, C.POINTER(C.c_uint8)), C.byref(olen), 0) == \
+        N.EINVAL
+    # the async entry needs an aligned result word
+    assert lib.paes_cuda_chunk_device_async(0, base, 256, 1, rk, base + 1024, None, 0, None) == N.EINVAL
+    assert lib.paes_cuda_chunk_device_async(0, base, 256, 1, rk, base + 1024, base + 2052, 0, None) == N.EINVAL
+    # a zero-length final decrypt is unpad_final's PaddingError, before any data is read
+    assert lib.paes_cuda_chunk_device_async(1, base, 0, 1, rk, base + 1024, res, 0, None) == N.EBADMSG
