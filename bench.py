@@ -662,6 +662,26 @@ class ConfigBench:
         self.s.synchronize()
         return statistics.mean(a.elapsed_time(b) for a, b in evs)
 
+    def graph_ms(self, fn, k):
+        """`k` calls captured once in a CUDA graph; ms per call of a replay."""
+        torch = self.torch
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.stream(self.s):
+            with torch.cuda.graph(g, stream=self.s):
+                for _ in range(k):
+                    fn()
+        with torch.cuda.stream(self.s):
+            g.replay()  # warm, on self.s (replay() launches on the current stream)
+        torch.cuda.synchronize(self.dev)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(self.s):
+            a.record(self.s)
+            g.replay()
+            b.record(self.s)
+        b.synchronize()
+        del g
+        return a.elapsed_time(b) / k
+
     def host_call(self, direction, src, n, final, rk, dst, steps):
         """paes_cuda_chunk on host pointers, synchronous; returns (GB/s of input, out_len)."""
         C, L = self.C, self.L
@@ -809,9 +829,17 @@ class ConfigBench:
                 del src, ct
             else:
                 steps = max(self.steps, 50)
-                ms = self.flushed(lambda: paes.chunk_device(0, src0.data_ptr(), n, True, rk, ct0.data_ptr(), self.dev,
-                                                            self.sp), steps)
+                call = lambda: paes.chunk_device(0, src0.data_ptr(), n, True, rk, ct0.data_ptr(), self.dev,  # noqa: E731
+                                                 self.sp)
+                ms = self.flushed(call, steps)
                 row["l2"] = "flushed before each call (256 MiB memset), per-call events"
+                # the same call back to back with the buffers L2-resident:
+                # issued one by one (host-issue bound), and replayed from a
+                # CUDA graph (device bound)
+                qms = self.queued([call] * (4 * steps))
+                gms = self.graph_ms(call, 4 * steps)
+                row.update(queued_gbs=round(n / qms / 1e6, 3), queued_us_per_call=round(qms * 1e3, 2),
+                           graph_gbs=round(n / gms / 1e6, 3), graph_us_per_call=round(gms * 1e3, 2))
             gbs = n / ms / 1e6
             row.update(device_gbs=round(gbs, 3), us_per_call=round(ms * 1e3, 2), pipe_frac=self.pipe_frac(gbs))
             hout = self.pinned(m)

@@ -92,7 +92,6 @@ int paes_cuda_set_pipeline(uint64_t chunk_bytes, int streams);
  * registered buffer is slow (2 GB/s), later calls are not; register with
  * cudaHostRegisterMapped, or set 0, to avoid it. */
 int paes_cuda_set_zero_copy_max(uint64_t bytes);
-
 /* ---- host-side rules (no GPU needed) ------------------------------------ */
 
 /* RoundKeySchedule(const Key128&) / expand_key (aes.hpp:39-50, aes.cpp:151-182). */

@@ -289,14 +289,17 @@ constexpr std::optional<ExecStrategy> strategy_from_string(std::string_view name
   return std::nullopt;
 }
 
+// Same members, order and defaults as the reference's JobSpec (exec.hpp:26-37),
+// so aggregate and designated initialisers written for it compile unchanged;
+// the Gpu strategy is opt-in, as a fourth ExecStrategy value would be.
 struct JobSpec {
   std::filesystem::path input_path;
   std::filesystem::path output_path;
   Key128 key;
-  unsigned workers = 1;  // GPUs; 0 = all visible
+  unsigned workers = 1;  // Gpu strategy: GPUs, 0 = all visible
+  ExecStrategy strategy = ExecStrategy::Sequential;
   Direction direction = Direction::Encrypt;
-  ExecStrategy strategy = ExecStrategy::Gpu;
-  std::filesystem::path worker_exe;  // unused by the gpu strategy (kept for source compatibility)
+  std::filesystem::path worker_exe;  // unused by the GPU pipeline (kept for source compatibility)
 };
 
 struct JobOutcome {

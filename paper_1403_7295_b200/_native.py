@@ -94,6 +94,8 @@ def lib_path() -> str:
 def load(build_if_missing: bool = False):
     """Load libpaes_cuda.so (in-tree).  Raises NativeLibraryMissing if absent."""
     global _lib
+    if _lib is not None:  # hot path: no lock once loaded
+        return _lib
     with _lock:
         if _lib is not None:
             return _lib

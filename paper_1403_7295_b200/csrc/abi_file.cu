@@ -72,6 +72,16 @@ void open_output(int fd, std::uint64_t cap, Map& map) {
     use_map = ::fstatfs(fd, &fs) == 0 && static_cast<unsigned long>(fs.f_type) == 0x01021994ul;  // TMPFS_MAGIC
   }
   if (!use_map) return;
+  // A store to a page of a shared mapping that the file system cannot back
+  // raises SIGBUS instead of returning ENOSPC, which would kill the process
+  // and leave the .part file behind.  Map only when the free space covers
+  // the whole output; otherwise pwrite, whose ENOSPC becomes IoError and the
+  // temp file is removed (AtomicOutput, exec.cpp:80-106).  (Reserving with
+  // fallocate instead was measured slower on tmpfs, see above.)
+  struct statfs fs {};
+  if (::fstatfs(fd, &fs) != 0 ||
+      static_cast<unsigned long long>(fs.f_bavail) * static_cast<unsigned long long>(fs.f_bsize) < cap)
+    return;
   void* p = ::mmap(nullptr, cap, PROT_READ | PROT_WRITE, MAP_SHARED, fd, 0);
   if (p != MAP_FAILED) {
     map.p = static_cast<std::uint8_t*>(p);
@@ -147,6 +157,9 @@ std::uint64_t file_shard(DevCtx& d, const Range& r, int in_fd, int out_fd, std::
                          const std::string& out_path, unsigned io_threads) {
   DeviceGuard g(d.id);
   ensure_pipeline(d, true);
+  // on an exception, drain the slots' streams before d.mu is released: a
+  // queued H2D may still read a pinned slot the next job would refill
+  QuiesceOnThrow quiesce{d};
   const int S = static_cast<int>(d.st.size());
   const std::uint64_t C = piece_size(r.in_len, d.chunk, S);
   const std::uint64_t npieces = std::max<std::uint64_t>(1, (r.in_len + C - 1) / C);
@@ -248,7 +261,7 @@ extern "C" int paes_cuda_run_job(const char* input_path, const char* output_path
     Map map;
     open_output(out.fd, cap, map);
     std::vector<std::uint64_t> produced(plan.size(), 0);
-    std::vector<std::string> failures(plan.size());
+    std::vector<std::string> failures(plan.size()), io_failures(plan.size());
     auto work = [&](std::size_t i) {
       const Chunk& c = plan[i];
       Range r;
@@ -267,7 +280,7 @@ extern "C" int paes_cuda_run_job(const char* input_path, const char* output_path
       } catch (const CudaFail& e) {
         failures[i] = e.msg;
       } catch (const IoFail& e) {
-        failures[i] = e.msg;
+        io_failures[i] = e.msg;
       } catch (const std::exception& e) {
         failures[i] = e.what();
       }
@@ -283,6 +296,10 @@ extern "C" int paes_cuda_run_job(const char* input_path, const char* output_path
         });
       for (auto& t : pool) t.join();
     }
+    // reading or writing the files is the reference's IoError (read_file /
+    // write_file, exec.cpp:48-76), whichever shard met it
+    for (const auto& m : io_failures)
+      if (!m.empty()) return fail(PAES_EIO, m);
     std::ostringstream failed;
     bool any = false;
     for (std::size_t i = 0; i < failures.size(); ++i) {

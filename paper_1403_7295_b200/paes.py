@@ -18,6 +18,7 @@ from __future__ import annotations
 
 import ctypes as C
 import os
+import threading
 from typing import Iterable, List
 
 from . import _native as N
@@ -331,12 +332,17 @@ def _job(direction: int, input: str, output: str, key: bytes, workers: int, stra
     return {"bytes_in": o.bytes_in, "bytes_out": o.bytes_out, "seconds": o.seconds}
 
 
-def encrypt_file(input: str, output: str, key: bytes, workers: int = 1, strategy: str = "gpu", worker_exe: str = ""):
-    """run_job(Encrypt) with ExecStrategy "gpu" (paes_module.cpp:95-109); workers = GPUs (0 = all)."""
+def encrypt_file(input: str, output: str, key: bytes, workers: int = 1, strategy: str = "sequential",
+                 worker_exe: str = ""):
+    """run_job(Encrypt) (paes_module.cpp:121-134), same defaults as the
+    reference: strategy "sequential" (one GPU, a bad trailer raises the bare
+    PaddingError); "gpu" takes workers = GPUs (0 = all)."""
     return _job(ENCRYPT, input, output, key, workers, strategy, worker_exe)
 
 
-def decrypt_file(input: str, output: str, key: bytes, workers: int = 1, strategy: str = "gpu", worker_exe: str = ""):
+def decrypt_file(input: str, output: str, key: bytes, workers: int = 1, strategy: str = "sequential",
+                 worker_exe: str = ""):
+    """run_job(Decrypt) (paes_module.cpp:136-149); defaults as encrypt_file."""
     return _job(DECRYPT, input, output, key, workers, strategy, worker_exe)
 
 
@@ -406,11 +412,20 @@ def ecb_device(direction: int, d_in: int, d_out: int, nbytes: int, rk: bytes, de
     _raise(N.load().paes_cuda_ecb_device(direction, d_in, d_out, nbytes, _rk176(rk), device, stream or None))
 
 
+_tls = threading.local()
+
+
 def chunk_device(direction: int, d_in: int, nbytes: int, is_final: bool, rk: bytes, d_out: int, device: int = 0,
                  stream: int = 0) -> int:
-    olen = C.c_uint64()
-    _raise(N.load().paes_cuda_chunk_device(direction, d_in, nbytes, int(bool(is_final)), _rk176(rk), d_out,
-                                           C.byref(olen), device, stream or None))
+    """encrypt_chunk / decrypt_chunk on device pointers (asynchronous on
+    `stream` except a final decrypt, which returns the unpadded length)."""
+    olen = getattr(_tls, "olen", None)
+    if olen is None:
+        olen = _tls.olen = C.c_uint64()
+    rc = N.load().paes_cuda_chunk_device(direction, d_in, nbytes, 1 if is_final else 0, _rk176(rk), d_out,
+                                         C.byref(olen), device, stream or None)
+    if rc:
+        _raise(rc)
     return olen.value
 
 
@@ -436,6 +451,8 @@ def _u64_array(xs):
 
 def _rk176(rk) -> bytes:
     """An expanded schedule crosses the ABI as a bare pointer: check its size here."""
+    if type(rk) is bytes and len(rk) == 176:
+        return rk
     rk = bytes(rk)
     if len(rk) != 176:
         raise ValueError("round keys must be the 176-byte expanded schedule (round_keys(key))")

@@ -107,17 +107,26 @@ static void host_tests() {
     CHECK(sb[static_cast<std::size_t>(x)] == s);
     CHECK(isb[sb[static_cast<std::size_t>(x)]] == x);
   }
+  // JobSpec: the reference's member order and defaults (exec.hpp:26-37), so its
+  // designated initialisers compile and a default JobSpec is Sequential
+  {
+    const gpu::JobSpec d{.input_path = "/tmp/a", .output_path = "/tmp/b", .key = gpu::Key128{}, .workers = 3,
+                         .strategy = gpu::ExecStrategy::Threaded, .direction = gpu::Direction::Decrypt,
+                         .worker_exe = "/bin/true"};
+    CHECK(d.workers == 3 && d.strategy == gpu::ExecStrategy::Threaded && d.direction == gpu::Direction::Decrypt);
+    CHECK(gpu::JobSpec{}.strategy == gpu::ExecStrategy::Sequential && gpu::JobSpec{}.workers == 1);
+  }
   // strategy names (exec.cpp:24-38) + "gpu"; the reference's worker-count rule (exec.cpp:209, 273)
   CHECK(gpu::to_string(gpu::ExecStrategy::Threaded) == "threads");
   CHECK(gpu::strategy_from_string("processes") == gpu::ExecStrategy::ProcessIsolated);
   CHECK(gpu::strategy_from_string("gpu") == gpu::ExecStrategy::Gpu);
   CHECK(!gpu::strategy_from_string("cuda").has_value());
   CHECK(throws<std::invalid_argument>([] {
-    gpu::JobSpec j{"/tmp/a", "/tmp/b", gpu::Key128{}, 0, gpu::Direction::Encrypt, gpu::ExecStrategy::Threaded, {}};
+    gpu::JobSpec j{"/tmp/a", "/tmp/b", gpu::Key128{}, 0, gpu::ExecStrategy::Threaded, gpu::Direction::Encrypt, {}};
     gpu::run_job(j);
   }));
   CHECK(throws<std::invalid_argument>([] {
-    gpu::JobSpec j{"/tmp/a", "/tmp/b", gpu::Key128{}, 0, gpu::Direction::Encrypt, gpu::ExecStrategy::ProcessIsolated,
+    gpu::JobSpec j{"/tmp/a", "/tmp/b", gpu::Key128{}, 0, gpu::ExecStrategy::ProcessIsolated, gpu::Direction::Encrypt,
                    {}};
     gpu::run_job(j);
   }));
@@ -213,10 +222,10 @@ static void gpu_tests() {
     f.write(reinterpret_cast<const char*>(big.data()), static_cast<std::streamsize>(big.size()));
   }
   gpu::JobSpec job{dir / "mb.bin", dir / "mb.enc", key_hex("000102030405060708090a0b0c0d0e0f"), 1,
-                   gpu::Direction::Encrypt};
+                   gpu::ExecStrategy::Gpu, gpu::Direction::Encrypt};
   const auto o = gpu::run_job(job);
   CHECK(o.bytes_in == (1u << 20) && o.bytes_out == (1u << 20) + 16);
-  gpu::JobSpec dec{dir / "mb.enc", dir / "mb.dec", job.key, 1, gpu::Direction::Decrypt};
+  gpu::JobSpec dec{dir / "mb.enc", dir / "mb.dec", job.key, 1, gpu::ExecStrategy::Gpu, gpu::Direction::Decrypt};
   CHECK(gpu::run_job(dec).bytes_out == (1u << 20));
   std::ifstream in(dir / "mb.dec", std::ios::binary);
   std::vector<std::uint8_t> got((std::istreambuf_iterator<char>(in)), std::istreambuf_iterator<char>());

@@ -4,6 +4,7 @@ the mapped bounce buffer for small pageable ranges and the staged ring for
 pageable memory -- all bit-exact vs the oracle across piece boundaries, and
 each rejecting a wrong key."""
 import ctypes as C
+import os
 import random
 
 import numpy as np
@@ -176,3 +177,32 @@ def test_staged_ring_large_pageable_matches_device_path(paes, gpu):
         assert np.array_equal(inplace[:m], want), n
         assert _run(paes, 1, inplace.ctypes.data, m, True, key, inplace.ctypes.data) == n
         assert np.array_equal(inplace[:n], src), n
+
+
+@pytest.mark.parametrize("writer", [None, "mmap", "pwrite"])
+def test_run_job_on_a_full_tmpfs_is_ioerror_without_partial_output(paes, gpu, tmp_path, writer, monkeypatch):
+    """An output tmpfs too small for the result: IoError (OSError), no SIGBUS
+    from the shared-mapping writer, and no <out>.part.<pid> left behind
+    (AtomicOutput, exec.cpp:80-106)."""
+    import subprocess
+
+    mnt = tmp_path / "small_tmpfs"
+    mnt.mkdir()
+    if subprocess.run(["mount", "-t", "tmpfs", "-o", "size=1m", "tmpfs", str(mnt)], capture_output=True).returncode:
+        pytest.skip("cannot mount a tmpfs here")
+    try:
+        if writer:
+            monkeypatch.setenv("PAES_FILE_WRITER", writer)
+        src = tmp_path / "in.bin"
+        src.write_bytes(os.urandom(4 << 20))
+        with pytest.raises(OSError) as ei:
+            paes.encrypt_file(str(src), str(mnt / "out.bin"), bytes(16), strategy="gpu")
+        assert isinstance(ei.value, paes.IoError), ei.value
+        assert os.listdir(mnt) == []
+        # the engine is still usable: a job that fits goes through
+        small = tmp_path / "small.bin"
+        small.write_bytes(os.urandom(100_000))
+        assert paes.encrypt_file(str(small), str(mnt / "ok.bin"), bytes(16))["bytes_out"] == 100_000 // 16 * 16 + 16
+        assert os.listdir(mnt) == ["ok.bin"]
+    finally:
+        subprocess.run(["umount", str(mnt)], capture_output=True)

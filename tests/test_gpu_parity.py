@@ -224,10 +224,16 @@ def test_file_roundtrip_and_failure(paes, gpu, orc, tmp_path):
     # empty file -> one pad block
     (tmp_path / "e.bin").write_bytes(b"")
     assert paes.encrypt_file(str(tmp_path / "e.bin"), str(tmp_path / "e.enc"), key)["bytes_out"] == 16
-    # wrong key: WorkerError naming the final chunk, no output left behind
+    # wrong key under strategy "gpu": WorkerError naming the final chunk, no
+    # output left behind; under the default strategy ("sequential", as in
+    # paes_module.cpp:134,149) the bare PaddingError, a ValueError
     bad = bytes([key[0] ^ 1]) + key[1:]
     with pytest.raises(paes.WorkerError, match="chunk 0"):
-        paes.decrypt_file(str(tmp_path / "c.bin"), str(tmp_path / "bad.bin"), bad, workers=1)
+        paes.decrypt_file(str(tmp_path / "c.bin"), str(tmp_path / "bad.bin"), bad, workers=1, strategy="gpu")
+    assert not (tmp_path / "bad.bin").exists()
+    with pytest.raises(ValueError) as ei:
+        paes.decrypt_file(str(tmp_path / "c.bin"), str(tmp_path / "bad.bin"), bad)
+    assert isinstance(ei.value, paes.PaddingError)
     assert not (tmp_path / "bad.bin").exists()
     assert not any(p.name.startswith("bad.bin.part") for p in tmp_path.iterdir())
     with pytest.raises(OSError):
@@ -502,13 +508,14 @@ def test_multi_shard_paths_on_one_device(paes, gpu, orc, tmp_path):
         # files: 3 shards, wrong key names the final chunk (exec.cpp:177-184)
         data = rnd.randbytes(200_001)
         (tmp_path / "p").write_bytes(data)
-        o = paes.encrypt_file(str(tmp_path / "p"), str(tmp_path / "c"), key, workers=3)
+        o = paes.encrypt_file(str(tmp_path / "p"), str(tmp_path / "c"), key, workers=3, strategy="gpu")
         assert o["bytes_out"] == (len(data) // 16 + 1) * 16
         assert (tmp_path / "c").read_bytes() == orc.encrypt_chunk(data, True, key)
-        paes.decrypt_file(str(tmp_path / "c"), str(tmp_path / "d"), key, workers=3)
+        paes.decrypt_file(str(tmp_path / "c"), str(tmp_path / "d"), key, workers=3, strategy="gpu")
         assert (tmp_path / "d").read_bytes() == data
         with pytest.raises(paes.WorkerError, match="chunk 2"):
-            paes.decrypt_file(str(tmp_path / "c"), str(tmp_path / "bad"), bytes([key[0] ^ 1]) + key[1:], workers=3)
+            paes.decrypt_file(str(tmp_path / "c"), str(tmp_path / "bad"), bytes([key[0] ^ 1]) + key[1:], workers=3,
+                              strategy="gpu")
         assert not (tmp_path / "bad").exists()
     finally:
         paes.set_devices([])

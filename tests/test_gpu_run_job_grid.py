@@ -33,7 +33,7 @@ def test_gpu_run_job_equals_reference_sequential(paes, gpu, ref, eight_workers, 
         expected = (tmp_path / "ref.enc").read_bytes()
         for workers in (1, 2, 3, 4, 8, 16, 32):
             out = tmp_path / "gpu.enc"
-            o = paes.encrypt_file(str(src), str(out), key, workers=workers)
+            o = paes.encrypt_file(str(src), str(out), key, strategy="gpu", workers=workers)
             assert o["bytes_in"] == size and o["bytes_out"] == len(expected)
             assert out.read_bytes() == expected, (size, workers)
 
@@ -45,9 +45,9 @@ def test_decrypt_inverts_encrypt_across_pairings(paes, gpu, ref, eight_workers, 
     src = tmp_path / "plain.bin"
     src.write_bytes(data)
     for enc_w in (1, 3):
-        paes.encrypt_file(str(src), str(tmp_path / "c.enc"), key, workers=enc_w)
+        paes.encrypt_file(str(src), str(tmp_path / "c.enc"), key, strategy="gpu", workers=enc_w)
         for dec_w in (1, 4, 8):
-            paes.decrypt_file(str(tmp_path / "c.enc"), str(tmp_path / "p.bin"), key, workers=dec_w)
+            paes.decrypt_file(str(tmp_path / "c.enc"), str(tmp_path / "p.bin"), key, strategy="gpu", workers=dec_w)
             assert (tmp_path / "p.bin").read_bytes() == data
         # and the reference's own threaded decrypt reads the GPU's ciphertext
         rc, _, bo, _ = ref.run_job(str(tmp_path / "c.enc"), str(tmp_path / "r.bin"), key, 4, 1, 1)
@@ -55,7 +55,7 @@ def test_decrypt_inverts_encrypt_across_pairings(paes, gpu, ref, eight_workers, 
     # wrong key with 4 workers: the final chunk (index 3) fails (test_exec.cpp:249-267)
     bad = bytes([key[0]]) + bytes([key[1] ^ 1]) + key[2:]
     with pytest.raises(paes.WorkerError, match="chunk 3"):
-        paes.decrypt_file(str(tmp_path / "c.enc"), str(tmp_path / "bad.bin"), bad, workers=4)
+        paes.decrypt_file(str(tmp_path / "c.enc"), str(tmp_path / "bad.bin"), bad, strategy="gpu", workers=4)
     assert not (tmp_path / "bad.bin").exists()
 
 
@@ -72,12 +72,12 @@ def test_acceptance_roundtrip_200_files(paes, gpu, ref, eight_workers, tmp_path)
         src.write_bytes(data)
         key = rnd.randbytes(16)
         w = 1 + i % 4
-        paes.encrypt_file(str(src), str(enc), key, workers=w)
+        paes.encrypt_file(str(src), str(enc), key, strategy="gpu", workers=w)
         ct = enc.read_bytes()
         for strategy, rw in ((0, 1), (1, w)):  # sequential, threads
             rc, _, _, _ = ref.run_job(str(src), str(tmp_path / "r.enc"), key, rw, strategy, 0)
             assert rc == 0 and (tmp_path / "r.enc").read_bytes() == ct, (i, size, strategy)
-        paes.decrypt_file(str(enc), str(back), key, workers=w)
+        paes.decrypt_file(str(enc), str(back), key, strategy="gpu", workers=w)
         assert back.read_bytes() == data, (i, size)
         rc, _, _, _ = ref.run_job(str(enc), str(back), key, w, 1, 1)
         assert rc == 0 and back.read_bytes() == data, (i, size)
@@ -103,9 +103,9 @@ def test_large_file_parallel_io_and_pwrite_path(paes, gpu, ref, eight_workers, t
     rc, _, _, _ = ref.run_job(str(src), str(tmp_path / "ref.enc"), key, 1, 0, 0)
     assert rc == 0
     for workers in (1, 2):
-        paes.encrypt_file(str(src), str(tmp_path / "gpu.enc"), key, workers=workers)
+        paes.encrypt_file(str(src), str(tmp_path / "gpu.enc"), key, strategy="gpu", workers=workers)
         assert (tmp_path / "gpu.enc").read_bytes() == (tmp_path / "ref.enc").read_bytes(), workers
-        paes.decrypt_file(str(tmp_path / "gpu.enc"), str(tmp_path / "back.bin"), key, workers=workers)
+        paes.decrypt_file(str(tmp_path / "gpu.enc"), str(tmp_path / "back.bin"), key, strategy="gpu", workers=workers)
         assert (tmp_path / "back.bin").read_bytes() == data, workers
 
 

@@ -306,3 +306,19 @@ def test_partial_overlap_is_rejected_before_any_device_work(lib):
     assert lib.paes_cuda_chunk_device_async(0, base, 256, 1, rk, base + 1024, base + 2052, 0, None) == N.EINVAL
     # a zero-length final decrypt is unpad_final's PaddingError, before any data is read
     assert lib.paes_cuda_chunk_device_async(1, base, 0, 1, rk, base + 1024, res, 0, None) == N.EBADMSG
+
+
+def test_product_library_links_no_reference_code():
+    """libpaes_cuda.so is built from this repo's sources only: none of the
+    reference's own symbols (paes::aes::*, paes::encrypt_chunk, ...) are in it,
+    and it does not depend on the reference build in oracle/_ref."""
+    import subprocess
+
+    from paper_1403_7295_b200 import _native
+
+    path = _native.lib_path()
+    syms = subprocess.run(["nm", "-C", path], capture_output=True, text=True).stdout
+    for bad in ("paes::aes::", "paes::encrypt_chunk", "paes::run_job", "paes::plan_chunks", "RoundKeySchedule"):
+        assert bad not in syms, bad
+    deps = subprocess.run(["ldd", path], capture_output=True, text=True).stdout
+    assert "paes_ref" not in deps and "_paes" not in deps
