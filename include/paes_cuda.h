@@ -102,6 +102,11 @@ int paes_cuda_expand_key(const uint8_t key[16], uint8_t rk[176]);
 int64_t paes_cuda_plan_chunks(uint64_t total_len, uint32_t workers, paes_chunk_spec* out, uint64_t cap);
 /* plan_decrypt_chunks (chunk.hpp:43-47, chunk.cpp:57-81). */
 int64_t paes_cuda_plan_decrypt_chunks(uint64_t cipher_len, uint32_t workers, paes_chunk_spec* out, uint64_t cap);
+/* Shards a host-pointer call or run_job with ngpus / workers = 0 uses over
+ * ndev listed GPUs: min(ndev, max(1, len / 8 MiB)) -- a short call stays on
+ * one GPU. */
+uint32_t paes_cuda_auto_shards(uint64_t len, uint32_t ndev);
+
 /* pad_final (chunk.hpp:49-50, chunk.cpp:83-88): out holds (len/16+1)*16 bytes;
  * in and out may alias.  Returns the padded length. */
 int64_t paes_cuda_pad_final(const uint8_t* raw, uint64_t len, uint8_t* out);
@@ -124,7 +129,8 @@ int paes_cuda_sbox(int inverse, uint8_t out[256]);
  * len must be a multiple of 16 (else PAES_EINVAL); in and out may alias
  * exactly.  Host pointers: the data is streamed H2D -> kernel -> D2H over
  * several CUDA streams per device and sharded over `ngpus` devices
- * (0 = all visible) as contiguous block ranges (the plan_chunks rule).
+ * (0 = all visible, at most one per 8 MiB: paes_cuda_auto_shards) as
+ * contiguous block ranges (the plan_chunks rule).
  * Synchronous. */
 int paes_cuda_ecb(int dir, const uint8_t* in, uint8_t* out, uint64_t len, const uint8_t rk[176], int ngpus);
 

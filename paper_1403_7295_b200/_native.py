@@ -55,6 +55,7 @@ SIGNATURES = [
     ("paes_cuda_sbox", C.c_int, [C.c_int, _vp]),
     ("paes_cuda_plan_chunks", C.c_int64, [_u64, C.c_uint32, C.POINTER(ChunkSpec), _u64]),
     ("paes_cuda_plan_decrypt_chunks", C.c_int64, [_u64, C.c_uint32, C.POINTER(ChunkSpec), _u64]),
+    ("paes_cuda_auto_shards", C.c_uint32, [_u64, C.c_uint32]),
     ("paes_cuda_pad_final", C.c_int64, [_vp, _u64, _vp]),
     ("paes_cuda_unpad_final", C.c_int64, [_vp, _u64]),
     ("paes_cuda_ecb", C.c_int, [C.c_int, _vp, _vp, _u64, _vp, C.c_int]),

@@ -85,6 +85,8 @@ int64_t paes_cuda_plan_decrypt_chunks(uint64_t cipher_len, uint32_t workers, pae
   return rc ? rc : n;
 }
 
+uint32_t paes_cuda_auto_shards(uint64_t len, uint32_t ndev) { return auto_shards(len, ndev); }
+
 int paes_cuda_sbox(int inverse, uint8_t out[256]) {
   if (!out) return fail(PAES_EINVAL, "null buffer");
   std::memcpy(out, inverse ? kTables.inv_sbox : kTables.sbox, 256);

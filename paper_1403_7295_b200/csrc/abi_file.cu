@@ -245,7 +245,7 @@ extern "C" int paes_cuda_run_job(const char* input_path, const char* output_path
     struct stat stt {};
     if (::fstat(in.fd, &stt) != 0) return fail(PAES_EIO, "cannot stat input: " + in_path);
     const std::uint64_t len = static_cast<std::uint64_t>(stt.st_size);
-    const auto devs = device_list(static_cast<int>(workers));
+    const auto devs = shard_devices(static_cast<int>(workers), len);
     const auto plan = dec ? plan_decrypt_chunks(len, static_cast<unsigned>(devs.size()))
                           : plan_chunks(len, static_cast<unsigned>(devs.size()));
     std::uint8_t rk[176];
@@ -288,13 +288,7 @@ extern "C" int paes_cuda_run_job(const char* input_path, const char* output_path
     if (plan.size() == 1) {
       work(0);
     } else {
-      std::vector<std::thread> pool;
-      for (std::size_t i = 0; i < plan.size(); ++i)
-        pool.emplace_back([&, i] {
-          bind_thread_to_device_numa(devs[i]);
-          work(i);
-        });
-      for (auto& t : pool) t.join();
+      shard_pool().run(std::vector<int>(devs.begin(), devs.begin() + static_cast<std::ptrdiff_t>(plan.size())), work);
     }
     // reading or writing the files is the reference's IoError (read_file /
     // write_file, exec.cpp:48-76), whichever shard met it

@@ -10,11 +10,20 @@
 // (run_process_isolated, exec.cpp:272-338) drives B200s when its
 // JobSpec::worker_exe points here: one process per chunk, one GPU each.
 // The chunk goes through paes_cuda_worker_chunk: the library's pipelined
-// file shard (parallel pread -> pinned ring -> kernel -> mapped output).  Device: --device, else PAES_WORKER_DEVICE, else the
-// chunk's index (offset / len) modulo the visible devices.
+// file shard (parallel pread -> pinned ring -> kernel -> mapped output).
+// Device: --device, else PAES_WORKER_DEVICE, else chunk i -> GPU i mod #GPUs.
+// The protocol passes no chunk index, but the parent names chunk i's output
+// "<output>.w<i>.<pid>.part" (exec.cpp:286-289), so i is read from --out.
+// (The byte range alone does not determine i: shares differ by one block --
+// 3,3,2,2 puts chunk 3 at offset / len = 4 -- and several worker counts can
+// produce the same range at different indices.)  Only an --out of another
+// shape falls back to offset / len.  --print-chunk-index prints i and exits
+// (no key, no GPU), for tests.
 //
 // Exit codes (paes_main.cpp:316-325): 0 ok, 2 invalid argument, 1 anything else.
 #include <unistd.h>
+
+#include <cctype>
 
 #include <cstdint>
 #include <cstdio>
@@ -31,6 +40,20 @@ int usage(const char* msg) {
   return 2;
 }
 
+// i from the parent's "<output>.w<i>.<pid>.part" (exec.cpp:286-289), else offset / len.
+std::uint64_t chunk_index(const std::string& out, std::uint64_t offset, std::uint64_t len) {
+  const std::size_t w = out.rfind(".w");
+  if (w != std::string::npos && out.size() > 5 && out.compare(out.size() - 5, 5, ".part") == 0) {
+    std::size_t i = w + 2, j = i;
+    while (j < out.size() && std::isdigit(static_cast<unsigned char>(out[j]))) ++j;
+    std::size_t k = j + 1, m = k;
+    while (m < out.size() && std::isdigit(static_cast<unsigned char>(out[m]))) ++m;
+    if (j > i && j < out.size() && out[j] == '.' && m > k && out.compare(m, std::string::npos, ".part") == 0)
+      return std::stoull(out.substr(i, j - i));
+  }
+  return len ? offset / len : 0;
+}
+
 }  // namespace
 
 int main(int argc, char** argv) {
@@ -38,8 +61,16 @@ int main(int argc, char** argv) {
   std::string in, out, dir;
   std::uint64_t offset = 0, len = 0;
   int final_flag = -1, keyfd = -1, device = -1;
-  for (int i = 2; i + 1 < argc; i += 2) {
-    const std::string k = argv[i], v = argv[i + 1];
+  bool print_index = false;
+  for (int i = 2; i < argc; i += 2) {
+    const std::string k = argv[i];
+    if (k == "--print-chunk-index") {
+      print_index = true;
+      --i;
+      continue;
+    }
+    if (i + 1 >= argc) return usage(("missing value for " + k).c_str());
+    const std::string v = argv[i + 1];
     try {
       if (k == "--in") in = v;
       else if (k == "--out") out = v;
@@ -53,6 +84,10 @@ int main(int argc, char** argv) {
     } catch (const std::exception&) {
       return usage(("bad value for " + k).c_str());
     }
+  }
+  if (print_index && !out.empty()) {
+    std::printf("%llu\n", static_cast<unsigned long long>(chunk_index(out, offset, len)));
+    return 0;
   }
   if (in.empty() || out.empty() || final_flag < 0 || keyfd < 0) return usage("missing option");
   int d = -1;
@@ -79,7 +114,7 @@ int main(int argc, char** argv) {
     return 1;
   }
   if (device < 0 && std::getenv("PAES_WORKER_DEVICE")) device = std::atoi(std::getenv("PAES_WORKER_DEVICE"));
-  if (device < 0) device = static_cast<int>((len ? offset / len : 0) % static_cast<std::uint64_t>(ndev));
+  if (device < 0) device = static_cast<int>(chunk_index(out, offset, len) % static_cast<std::uint64_t>(ndev));
   if (paes_cuda_set_devices(&device, 1) != PAES_OK) {
     std::fprintf(stderr, "worker: %s\n", paes_cuda_last_error());
     return 1;

@@ -95,6 +95,11 @@ std::vector<Chunk> plan_decrypt_chunks(std::uint64_t cipher_len, unsigned worker
   return plan;
 }
 
+unsigned auto_shards(std::uint64_t len, unsigned ndev) {
+  const std::uint64_t by_size = std::max<std::uint64_t>(1, len / kMinShardBytes);
+  return static_cast<unsigned>(std::min<std::uint64_t>(std::max(1u, ndev), by_size));
+}
+
 std::uint64_t unpad_final(const std::uint8_t* padded, std::uint64_t len) {
   if (len == 0 || len % 16 != 0) throw PaddingError("unpad: length must be a non-zero multiple of 16");
   const std::uint8_t k = padded[len - 1];

@@ -35,6 +35,12 @@ KeyWords dec_key_words(const std::uint8_t rk[176]);
 std::vector<Chunk> plan_chunks(std::uint64_t total_len, unsigned workers);
 std::vector<Chunk> plan_decrypt_chunks(std::uint64_t cipher_len, unsigned workers);
 
+// Shards a host-pointer call over `ndev` listed devices when the caller lets
+// the library choose (ngpus = 0): at most one per kMinShardBytes of input,
+// so a short call stays on one GPU instead of paying N launches and syncs.
+constexpr std::uint64_t kMinShardBytes = 8ull << 20;
+unsigned auto_shards(std::uint64_t len, unsigned ndev);
+
 // unpad_final (chunk.cpp:90-100): unpadded length, throws PaddingError.
 std::uint64_t unpad_final(const std::uint8_t* padded, std::uint64_t len);
 

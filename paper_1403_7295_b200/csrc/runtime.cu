@@ -265,6 +265,63 @@ std::vector<int> device_list(int ngpus) {
   return list;
 }
 
+std::vector<int> shard_devices(int ngpus, std::uint64_t len) {
+  std::vector<int> devs = device_list(ngpus);
+  if (ngpus == 0) devs.resize(auto_shards(len, static_cast<unsigned>(devs.size())));
+  return devs;
+}
+
+void ShardPool::loop(Worker* w) {
+  int bound = -1;
+  for (;;) {
+    std::function<void()> job;
+    int dev;
+    {
+      std::unique_lock<std::mutex> lk(w->mu);
+      w->cv.wait(lk, [w] { return static_cast<bool>(w->job); });
+      job = std::move(w->job);
+      w->job = nullptr;
+      dev = w->dev;
+    }
+    if (dev != bound) {
+      bind_thread_to_device_numa(dev);
+      bound = dev;
+    }
+    job();
+    {
+      std::lock_guard<std::mutex> lk(done_mu_);
+      if (--pending_ == 0) done_cv_.notify_all();
+    }
+  }
+}
+
+void ShardPool::run(const std::vector<int>& devs, const std::function<void(std::size_t)>& f) {
+  std::lock_guard<std::mutex> call(call_mu_);
+  while (workers_.size() < devs.size()) {
+    workers_.push_back(std::make_unique<Worker>());
+    Worker* w = workers_.back().get();
+    w->th = std::thread([this, w] { loop(w); });
+  }
+  {
+    std::lock_guard<std::mutex> lk(done_mu_);
+    pending_ = devs.size();
+  }
+  for (std::size_t k = 0; k < devs.size(); ++k) {
+    Worker& w = *workers_[k];
+    std::lock_guard<std::mutex> lk(w.mu);
+    w.dev = devs[k];
+    w.job = [&f, k] { f(k); };
+    w.cv.notify_one();
+  }
+  std::unique_lock<std::mutex> lk(done_mu_);
+  done_cv_.wait(lk, [this] { return pending_ == 0; });
+}
+
+ShardPool& shard_pool() {
+  static ShardPool* pool = new ShardPool();  // leaked on purpose: parked threads outlive static destructors
+  return *pool;
+}
+
 EcbArgs make_args(const Range& r, const std::uint8_t* in, std::uint8_t* out, std::uint64_t in_len, bool last,
                   const KeyWords& kw, std::uint32_t* status) {
   EcbArgs a{};
@@ -688,7 +745,7 @@ int host_transform(int dir, const std::uint8_t* in, std::uint64_t len, bool is_f
   }
   if (!out) throw std::invalid_argument("null output");
   check_alias(in, len, out, (is_final && !dec) ? (len / 16 + 1) * 16 : len);
-  const auto devs = device_list(ngpus);
+  const auto devs = shard_devices(ngpus, len);
   const KeyWords kw = dec ? dec_key_words(rk) : enc_key_words(rk);
   const auto plan = dec ? plan_decrypt_chunks(len, static_cast<unsigned>(devs.size()))
                         : plan_chunks(len, static_cast<unsigned>(devs.size()));
@@ -712,14 +769,8 @@ int host_transform(int dir, const std::uint8_t* in, std::uint64_t len, bool is_f
   };
   if (plan.size() == 1) {
     work(0);
-  } else {  // one library-owned thread per shard, on its GPU's NUMA node
-    std::vector<std::thread> pool;
-    for (std::size_t i = 0; i < plan.size(); ++i)
-      pool.emplace_back([&, i] {
-        bind_thread_to_device_numa(devs[i]);
-        work(i);
-      });
-    for (auto& t : pool) t.join();
+  } else {  // one persistent library thread per shard, on its GPU's NUMA node
+    shard_pool().run(std::vector<int>(devs.begin(), devs.begin() + static_cast<std::ptrdiff_t>(plan.size())), work);
   }
   for (std::size_t i = 0; i < plan.size(); ++i)
     if (codes[i]) return fail(codes[i], msgs[i]);

@@ -10,6 +10,7 @@
 #include <condition_variable>
 #include <cstdint>
 #include <exception>
+#include <functional>
 #include <memory>
 #include <mutex>
 #include <stdexcept>
@@ -180,8 +181,39 @@ struct QuiesceOnThrow {
       for (auto s : d.st) cudaStreamSynchronize(s);
   }
 };
-// The devices host-pointer calls shard over (first `ngpus`, 0 = all).
+// Persistent host threads for multi-shard calls (a fresh
+// std::thread per shard per call cost tens of microseconds).  run() hands
+// shard k to pool thread k, which binds itself to the NUMA node of the
+// device it serves (re-binding only when that changes), and returns when
+// every shard is done.  Multi-shard calls from several host threads take
+// turns; they would serialise on the devices' locks anyway.  f must not
+// throw (callers wrap their shard work in guarded()).
+class ShardPool {
+ public:
+  void run(const std::vector<int>& devs, const std::function<void(std::size_t)>& f);
+
+ private:
+  struct Worker {
+    std::thread th;
+    std::mutex mu;
+    std::condition_variable cv;
+    std::function<void()> job;
+    int dev = -1;
+  };
+  void loop(Worker* w);
+  std::mutex call_mu_;
+  std::vector<std::unique_ptr<Worker>> workers_;
+  std::mutex done_mu_;
+  std::condition_variable done_cv_;
+  std::size_t pending_ = 0;
+};
+// The process-wide pool (never destroyed: its threads park until exit).
+ShardPool& shard_pool();
+
+// The devices host-pointer calls shard over (first `ngpus`; 0 = all listed,
+// at most one per kMinShardBytes of `len`).
 std::vector<int> device_list(int ngpus);
+std::vector<int> shard_devices(int ngpus, std::uint64_t len);
 void set_device_list(const std::vector<int>& ids);
 void set_pipeline_config(std::uint64_t chunk_bytes, int streams);
 void set_zero_copy_max(std::uint64_t bytes);

@@ -42,10 +42,11 @@ def _worker(rank, world, port, total, out_dir):
     total_cs = bench.sum_checksums(d, cs)
     t_max = d.reduce(float(rank + 1), "max")
     n_all = d.reduce(int(sh["raw_len"]), "sum")
+    per_rank = d.gather(float(10 * rank + 1))  # bench.py's per-rank fields
     with open(os.path.join(out_dir, f"r{rank}.bin"), "wb") as f:
         f.write(ct)
     with open(os.path.join(out_dir, f"r{rank}.txt"), "w") as f:
-        f.write(f"{total_cs} {t_max} {n_all}")
+        f.write(f"{total_cs} {t_max} {n_all} {','.join(str(x) for x in per_rank)}")
     d.barrier()
     d.close()
 
@@ -60,7 +61,8 @@ def test_two_rank_shards_stitch_to_whole(tmp_path, total, orc):
     assert stitched == whole  # output offsets == input offsets: no assemble step
     want_cs = orc.checksum(whole[: len(whole) - len(whole) % 8], 0)
     for r in range(world):
-        cs, tmax, n_all = (tmp_path / f"r{r}.txt").read_text().split()
+        cs, tmax, n_all, per_rank = (tmp_path / f"r{r}.txt").read_text().split()
+        assert [float(x) for x in per_rank.split(",")] == [1.0, 11.0]
         assert int(cs) == want_cs
         assert float(tmax) == 2.0
         assert int(n_all) == total

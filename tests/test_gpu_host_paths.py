@@ -206,3 +206,25 @@ def test_run_job_on_a_full_tmpfs_is_ioerror_without_partial_output(paes, gpu, tm
         assert os.listdir(mnt) == ["ok.bin"]
     finally:
         subprocess.run(["umount", str(mnt)], capture_output=True)
+
+
+def test_short_calls_stay_on_one_listed_gpu(paes, gpu, orc):
+    """With three devices listed and ngpus = 0, a 1 KiB call is one shard, one
+    launch (the size floor); 40 MiB shards three ways and still matches the
+    oracle (the shard threads are the persistent pool's)."""
+    rnd = random.Random(77)
+    key = rnd.randbytes(16)
+    paes.set_devices([0, 0, 0])
+    try:
+        small = rnd.randbytes(1024)
+        before = paes.launch_count()
+        ct = paes.encrypt_bytes(small, key)
+        assert paes.launch_count() - before == 1
+        assert ct == orc.encrypt_chunk(small, True, key)
+        big = rnd.randbytes((40 << 20) + 5)
+        for _ in range(3):  # pool threads are reused across calls
+            ct = paes.encrypt_chunk(big, True, key)
+            assert ct == orc.encrypt_chunk(big, True, key, threads=4)
+            assert paes.decrypt_chunk(ct, True, key) == big
+    finally:
+        paes.set_devices([])
