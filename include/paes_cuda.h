@@ -207,6 +207,14 @@ typedef struct paes_batch_plan paes_batch_plan;
 int paes_cuda_batch_plan_create(int dir, const uint64_t* in_off, const uint64_t* out_off, const uint64_t* lens,
                                 const uint8_t* rks, uint32_t n, int pad, int device, paes_batch_plan** plan);
 int paes_cuda_batch_plan_run(paes_batch_plan* plan, const void* d_in, void* d_out, uint64_t* out_lens, void* stream);
+/* Queued form of paes_cuda_batch_plan_run: never synchronises (CUDA-graph
+ * capturable) and may run concurrently with other runs of the plan.  When
+ * the kernel has run, d_out_lens[i] (n uint64 words in device memory or
+ * mapped pinned memory, 8-byte aligned) holds message i's output length --
+ * unpadded for a checked decrypt -- or PAES_BAD_PAD for a malformed
+ * trailer. */
+int paes_cuda_batch_plan_run_async(paes_batch_plan* plan, const void* d_in, void* d_out, uint64_t* d_out_lens,
+                                   void* stream);
 void paes_cuda_batch_plan_destroy(paes_batch_plan* plan);
 
 /* ---- file path: ExecStrategy "gpu" for run_job (exec.hpp:18-45) ---------

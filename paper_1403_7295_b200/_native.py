@@ -70,6 +70,7 @@ SIGNATURES = [
     ("paes_cuda_batch_plan_create", C.c_int, [C.c_int, C.POINTER(_u64), C.POINTER(_u64), C.POINTER(_u64), _vp,
                                               C.c_uint32, C.c_int, C.c_int, C.POINTER(_vp)]),
     ("paes_cuda_batch_plan_run", C.c_int, [_vp, _vp, _vp, C.POINTER(_u64), _vp]),
+    ("paes_cuda_batch_plan_run_async", C.c_int, [_vp, _vp, _vp, _vp, _vp]),
     ("paes_cuda_batch_plan_destroy", None, [_vp]),
     ("paes_cuda_run_job", C.c_int, [C.c_char_p, C.c_char_p, _vp, C.c_uint32, C.c_int, C.POINTER(JobOutcome)]),
     ("paes_cuda_sweep", C.c_int, [_u64, _u64, _vp]),
@@ -107,6 +108,14 @@ def load(build_if_missing: bool = False):
             else:
                 raise NativeLibraryMissing(
                     f"{path} is not built; run `python -m paper_1403_7295_b200.build` (no CPU fallback exists)")
+        elif "PAES_CUDA_LIB" not in os.environ and _build._stale():
+            # never rebuild behind the caller's back (a variant or a copied
+            # tree may have skewed mtimes); say that the kernels may be old
+            import warnings
+
+            warnings.warn(f"{path} is older than its sources in {_build.CSRC}; rebuild with "
+                          "`python -m paper_1403_7295_b200.build` to load the current kernels", RuntimeWarning,
+                          stacklevel=2)
         L = C.CDLL(path)
         for name, res, args in SIGNATURES:
             fn = getattr(L, name)

@@ -27,6 +27,7 @@ struct BatchImage {
   std::uint32_t n = 0;
   unsigned long long total_tiles = 0;  // warp tiles (each message owns whole tiles)
   std::size_t msg_bytes = 0, keys_off = 0, image_bytes = 0, status_off = 0, total_bytes = 0;
+  bool has_empty = false;  // some message has no output block (its length is written by the host)
   std::vector<std::uint64_t> lens;
   std::vector<std::uint32_t> nblocks;
 };
@@ -55,6 +56,7 @@ BatchImage plan_batch(int dir, const uint64_t* in_off, const uint64_t* out_off, 
     if (lens[i] > UINT64_MAX - in_off[i] || 16 * nb > UINT64_MAX - out_off[i])
       throw std::invalid_argument("batch message span overflows the address range");
     b.nblocks[i] = static_cast<std::uint32_t>(nb);
+    if (nb == 0) b.has_empty = true;
     b.total_tiles += (nb + batch_tile_blocks() - 1) / batch_tile_blocks();
   }
   return b;
@@ -271,6 +273,28 @@ int paes_cuda_batch_plan_run(paes_batch_plan* plan, const void* d_in, void* d_ou
     PAES_CK(cudaMemcpyAsync(plan->h_status, plan->dd + b.status_off, 4ull * b.n, cudaMemcpyDeviceToHost, s));
     PAES_CK(cudaStreamSynchronize(s));
     finish_lengths(b, plan->h_status, out_lens);
+    return PAES_OK;
+  });
+}
+
+int paes_cuda_batch_plan_run_async(paes_batch_plan* plan, const void* d_in, void* d_out, uint64_t* d_out_lens,
+                                   void* stream) {
+  return guarded([&] {
+    if (!plan) throw std::invalid_argument("null plan");
+    if (!d_out_lens || reinterpret_cast<std::uintptr_t>(d_out_lens) % 8)
+      throw std::invalid_argument("d_out_lens must be an 8-byte aligned device-visible array");
+    const BatchImage& b = plan->img;
+    if (b.n == 0) return PAES_OK;
+    if (!d_in || !d_out) throw std::invalid_argument("null device buffer");
+    DevCtx& d = device(plan->device);
+    DeviceGuard dg(plan->device);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    // messages without an output block own no tile, so no thread writes them
+    if (b.has_empty) PAES_CK(cudaMemsetAsync(d_out_lens, 0, 8ull * b.n, s));
+    BatchArgs a = batch_args(b, d_in, d_out, plan->dd);
+    a.status = nullptr;  // the verdicts go to the caller's array: runs never share state
+    a.out_lens = reinterpret_cast<unsigned long long*>(d_out_lens);
+    PAES_CK(launch_batch(b.dec, a, d.sm_count, s));
     return PAES_OK;
   });
 }

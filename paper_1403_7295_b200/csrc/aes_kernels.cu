@@ -388,6 +388,11 @@ template <bool DEC, int NB, bool ALIGNED>
 __global__ void __launch_bounds__(kThreads, 1) batch_kernel(const __grid_constant__ BatchArgs a) {
   extern __shared__ __align__(16) std::uint32_t sm[];
   stage_tables<DEC>(sm);
+  // programmatic dependent launch, as in ecb_kernel: the staging above
+  // overlaps the previous kernel's tail; descriptors and data are touched
+  // only after it has completed
+  asm volatile("griddepcontrol.launch_dependents;");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   __syncthreads();
   const char* smb = reinterpret_cast<const char*>(sm);
   const std::uint32_t lane = threadIdx.x & 31;
@@ -434,9 +439,11 @@ __global__ void __launch_bounds__(kThreads, 1) batch_kernel(const __grid_constan
         kw[4 * i + 3] = v.w;
       }
     }
-    // tiles of whole input blocks; the tile holding a checked trailer goes to
-    // the ragged loop so the pad check always runs
-    const unsigned long long whole = msg.nfull >= a.check_pad ? (msg.nfull - a.check_pad) / kTile : 0;
+    // tiles of whole input blocks; the tile holding the message's last block
+    // goes to the ragged loop when the trailer is checked or the length
+    // reported, so the thread that owns that block runs the epilogue
+    const unsigned long long excl = ((a.check_pad || a.out_lens) && msg.nblocks == msg.nfull) ? 1 : 0;
+    const unsigned long long whole = msg.nfull >= excl ? (msg.nfull - excl) / kTile : 0;
     const unsigned long long full_end = min(msg_end, msg.first_tile + whole);
     const unsigned long long t0 = (tile - msg.first_tile) * kTile + lane;  // lane's first block in the message
     const std::uint8_t* src = a.in + msg.in_off + 16ull * t0;
@@ -483,7 +490,15 @@ __global__ void __launch_bounds__(kThreads, 1) batch_kernel(const __grid_constan
         const unsigned long long lb = tb + 32ull * j;
         if (lb < msg.nblocks) {
           store_block<ALIGNED>(mdst + 16ull * lb, s[j]);
-          if (DEC && a.check_pad && lb == msg.nblocks - 1) a.status[m] = pad_check(s[j]);
+          if (lb == msg.nblocks - 1) {
+            unsigned long long olen = 16ull * msg.nblocks;
+            if (DEC && a.check_pad) {
+              const std::uint32_t k = pad_check(s[j]);
+              if (a.status) a.status[m] = k;
+              olen = k == 0xffffffffu ? ~0ull : olen - k;
+            }
+            if (a.out_lens) a.out_lens[m] = olen;
+          }
         }
       }
     }
@@ -670,10 +685,11 @@ cudaError_t launch_batch(bool dec, const BatchArgs& args, int sm_count, cudaStre
   const int smem = dec ? kDecLaunchSmem : kEncLaunchSmem;
   const bool aligned =
       args.aligned && ((reinterpret_cast<std::uintptr_t>(args.in) | reinterpret_cast<std::uintptr_t>(args.out)) & 15) == 0;
-  if (dec) return aligned ? launch_k(batch_kernel<true, kNB, true>, grid, kThreads, smem, stream, false, args)
-                          : launch_k(batch_kernel<true, kNB, false>, grid, kThreads, smem, stream, false, args);
-  return aligned ? launch_k(batch_kernel<false, kNB, true>, grid, kThreads, smem, stream, false, args)
-                 : launch_k(batch_kernel<false, kNB, false>, grid, kThreads, smem, stream, false, args);
+  const bool pdl = PAES_PDL != 0;
+  if (dec) return aligned ? launch_k(batch_kernel<true, kNB, true>, grid, kThreads, smem, stream, pdl, args)
+                          : launch_k(batch_kernel<true, kNB, false>, grid, kThreads, smem, stream, pdl, args);
+  return aligned ? launch_k(batch_kernel<false, kNB, true>, grid, kThreads, smem, stream, pdl, args)
+                 : launch_k(batch_kernel<false, kNB, false>, grid, kThreads, smem, stream, pdl, args);
 }
 
 cudaError_t launch_state_op(int op, std::uint8_t* d_states, unsigned long long n, const StateKey& rk,

@@ -101,7 +101,8 @@ struct BatchArgs {
   std::uint8_t* out;
   const BatchMsg* msgs;
   const std::uint32_t* keys;         // 44 words per message, in order of use
-  std::uint32_t* status;             // decrypt+pad: one word per message
+  std::uint32_t* status;             // decrypt+pad: one word per message (nullable)
+  unsigned long long* out_lens;      // nullable: per-message output length (~0 = bad trailer), device-visible
   unsigned long long total_tiles;
   std::uint32_t nmsg;
   std::uint32_t check_pad;

@@ -518,6 +518,12 @@ class BatchPlan:
                                                  stream or None))
         return olens[: self.n].tolist()
 
+    def run_async(self, d_in: int, d_out: int, d_out_lens: int, stream: int = 0) -> None:
+        """Queued run (paes_cuda_batch_plan_run_async): no sync, graph-capturable;
+        the n uint64 words at ``d_out_lens`` receive the output lengths
+        (``BAD_PAD`` for a malformed trailer) when the kernel has run."""
+        _raise(N.load().paes_cuda_batch_plan_run_async(self._h, d_in, d_out, d_out_lens, stream or None))
+
     def close(self):
         if getattr(self, "_h", None) is not None and self._h.value:
             N.load().paes_cuda_batch_plan_destroy(self._h)

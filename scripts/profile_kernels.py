@@ -1,8 +1,9 @@
-"""Small driver for ncu: one launch each of the encrypt, decrypt and batch
-kernels on 1 GiB of device-generated data (plus warm-up launches).
+"""Small driver for ncu: one launch each of the encrypt, decrypt, batch
+encrypt and batch decrypt kernels on 1 GiB of device-generated data (plus
+warm-up launches).
 
     python scripts/profile_kernels.py
-    ncu --set full --clock-control none -k regex:"ecb_kernel|batch_kernel" -s 3 -c 3 -o prof python scripts/profile_kernels.py
+    ncu --set full --clock-control none -k regex:"ecb_kernel|batch_kernel" -s 4 -c 4 -o prof python scripts/profile_kernels.py
 """
 import os
 import sys
@@ -31,15 +32,18 @@ for L in lens:
 rks = np.frombuffer(os.urandom(16 * len(L2)), dtype=np.uint8)
 rk_all = b"".join(paes.round_keys(bytes(rks[16 * i:16 * i + 16])) for i in range(len(L2)))
 plan = paes.BatchPlan(0, in_off, out_off, L2, rk_all, True)
+dplan = paes.BatchPlan(1, out_off, in_off, [x + 16 for x in L2], rk_all, True)
 # warm-up: one of each
 paes.ecb_device(0, a.data_ptr(), b.data_ptr(), n, rk)
 paes.ecb_device(1, b.data_ptr(), a.data_ptr(), n, rk)
 plan.run(a.data_ptr(), b.data_ptr())
+dplan.run(b.data_ptr(), a.data_ptr())
 torch.cuda.synchronize()
 # profiled: encrypt, decrypt, batch encrypt (x3 each when sizing a launch list)
 for _ in range(3 if len(sys.argv) > 1 else 1):
     paes.ecb_device(0, a.data_ptr(), b.data_ptr(), n, rk)
     paes.ecb_device(1, b.data_ptr(), a.data_ptr(), n, rk)
     plan.run(a.data_ptr(), b.data_ptr())
+    dplan.run(b.data_ptr(), a.data_ptr())
 torch.cuda.synchronize()
 print("ok", len(L2), "messages")

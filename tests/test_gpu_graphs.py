@@ -152,3 +152,59 @@ def test_async_result_word_in_mapped_memory_and_empty_inputs(paes, gpu):
         paes.chunk_device_async(paes.DECRYPT, ct.data_ptr(), 0, True, rk, ct.data_ptr(), hp, 0, s.cuda_stream)
     with pytest.raises(ValueError):
         paes.chunk_device_async(paes.ENCRYPT, ct.data_ptr(), 16, True, rk, ct.data_ptr(), hp + 4, 0, s.cuda_stream)
+
+
+def test_batch_plan_run_async_lengths_and_bad_trailers(paes, gpu, orc):
+    """Queued batch decrypt: per-message unpadded lengths land in a device
+    array, malformed trailers (wrong keys) as BAD_PAD at exactly those
+    messages, empty messages as 0; the run replays from a CUDA graph."""
+    import torch
+
+    rnd = random.Random(12)
+    lens = [rnd.randrange(0, 50_000) for _ in range(40)]
+    keys = [rnd.randbytes(16) for _ in lens]
+    msgs = [rnd.randbytes(L) for L in lens]
+    cts = [orc.encrypt_chunk(m, True, k) for m, k in zip(msgs, keys)]
+    bad = {3, 17, 29}
+    rks = b"".join(paes.round_keys(bytes(16) if i in bad else k) for i, k in enumerate(keys))
+    off, o = [], 0
+    for c in cts:
+        off.append(o)
+        o += len(c)
+    src = torch.frombuffer(bytearray(b"".join(cts)), dtype=torch.uint8).cuda()
+    dst = torch.zeros(o + 16, dtype=torch.uint8, device="cuda")
+    res = torch.full((len(lens),), -7, dtype=torch.int64, device="cuda")
+    plan = paes.BatchPlan(paes.DECRYPT, off, off, [len(c) for c in cts], rks, True)
+    try:
+        s = torch.cuda.Stream()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.stream(s):
+            plan.run_async(src.data_ptr(), dst.data_ptr(), res.data_ptr(), s.cuda_stream)
+            s.synchronize()
+            with torch.cuda.graph(g, stream=s):
+                plan.run_async(src.data_ptr(), dst.data_ptr(), res.data_ptr(), s.cuda_stream)
+        for rep in range(2):
+            res.fill_(-7)
+            torch.cuda.synchronize()
+            g.replay()
+            torch.cuda.synchronize()
+            got = [int(x) & ((1 << 64) - 1) for x in res.tolist()]
+            out = dst.cpu().numpy().tobytes()
+            for i, (m, c) in enumerate(zip(msgs, cts)):
+                if i in bad:
+                    u = orc.unpad(orc.ecb(1, c[-16:], bytes(16)))
+                    assert got[i] == (paes.BAD_PAD if u < 0 else len(c) - 16 + u), (rep, i)
+                else:
+                    assert got[i] == len(m), (rep, i)
+                    assert out[off[i]:off[i] + len(m)] == m, (rep, i)
+    finally:
+        plan.close()
+    # an encrypt plan with an empty, unpadded message: its length is 0
+    enc = paes.BatchPlan(paes.ENCRYPT, [0, 0], [0, 32], [0, 32], rks[:352], False)
+    try:
+        r2 = torch.full((2,), -7, dtype=torch.int64, device="cuda")
+        enc.run_async(src.data_ptr(), dst.data_ptr(), r2.data_ptr())
+        torch.cuda.synchronize()
+        assert r2.tolist() == [0, 32]
+    finally:
+        enc.close()

@@ -40,6 +40,31 @@ def to_bytes(t, start: int, n: int) -> bytes:
     return t[start:start + n].cpu().numpy().tobytes()
 
 
+def sha256_device(t, n: int, piece: int = 1 << 30) -> str:
+    """SHA-256 of t[:n] (device): D2H of piece k+1 into one pinned buffer
+    while piece k is hashed from the other (hashlib releases the GIL)."""
+    import threading
+
+    torch = _torch()
+    h = hashlib.sha256()
+    bufs = [torch.empty(piece, dtype=torch.uint8, pin_memory=True) for _ in range(2)]
+    s = torch.cuda.Stream()
+    worker = None
+    for k, off in enumerate(range(0, n, piece)):
+        m = min(piece, n - off)
+        b = bufs[k % 2]  # last read by hasher k-2, already joined
+        with torch.cuda.stream(s):
+            b[:m].copy_(t[off:off + m], non_blocking=True)
+        s.synchronize()
+        if worker:
+            worker.join()
+        worker = threading.Thread(target=h.update, args=(b[:m].numpy(),))
+        worker.start()
+    if worker:
+        worker.join()
+    return h.hexdigest()
+
+
 # ------------------------------------------------------------ KATs / golden
 def test_block_kats(paes, gpu, golden):
     """FIPS-197 B and C.1 + zero-key decrypt snapshot (test_aes.cpp:255-292)."""
@@ -385,6 +410,9 @@ def test_config4_64gib_device_generated(paes, gpu, digests):
     for off, h in d["window_sha256"].items():
         off = int(off)
         assert hashlib.sha256(to_bytes(ct, off, W)).hexdigest() == h, off
+    # the full SHA-256 of all 64 GiB + 16 ciphertext bytes, against the one the
+    # reference's own encrypt path produced (tests/golden/make_cfg4_sha256.py)
+    assert sha256_device(ct, total + 16) == d["ct_sha256"]
     # round trip in place over the plaintext buffer
     assert paes.chunk_device(1, ct.data_ptr(), total + 16, True, rk, pt.data_ptr()) == total
     assert paes.checksum_device(pt.data_ptr(), total, 0) == d["pt_checksum"]

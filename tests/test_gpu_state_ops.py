@@ -15,9 +15,8 @@ def test_all_ops_vs_oracle(paes, gpu, orc):
     rk = rnd.randbytes(16)
     for op in range(7):
         got = paes.state_transform(op, states, rk if op == paes.ADD_ROUND_KEY else None)
-        for i in range(0, n, 97):  # every 97th state through the (slow, per-state) oracle
-            s = states[16 * i:16 * i + 16]
-            assert got[16 * i:16 * i + 16] == orc.transform(op, s, rk), (op, i)
+        want = b"".join(orc.transform(op, states[16 * i:16 * i + 16], rk) for i in range(n))
+        assert got == want, op  # every one of the 20000 states
     # inverses round-trip every state
     for fwd, inv in ((paes.SUB_BYTES, paes.INV_SUB_BYTES), (paes.SHIFT_ROWS, paes.INV_SHIFT_ROWS),
                      (paes.MIX_COLUMNS, paes.INV_MIX_COLUMNS)):

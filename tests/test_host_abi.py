@@ -322,3 +322,21 @@ def test_product_library_links_no_reference_code():
         assert bad not in syms, bad
     deps = subprocess.run(["ldd", path], capture_output=True, text=True).stdout
     assert "paes_ref" not in deps and "_paes" not in deps
+
+
+def test_stale_library_warns_instead_of_loading_silently(monkeypatch):
+    """load() says when libpaes_cuda.so is older than its sources (it never
+    rebuilds behind the caller's back)."""
+    import warnings
+
+    from paper_1403_7295_b200 import _native
+    from paper_1403_7295_b200 import build as B
+
+    monkeypatch.setattr(_native, "_lib", None)
+    monkeypatch.delenv("PAES_CUDA_LIB", raising=False)
+    monkeypatch.setattr(B, "_stale", lambda: True)
+    with warnings.catch_warnings(record=True) as w:
+        warnings.simplefilter("always")
+        L = _native.load()
+    assert L is not None
+    assert any("older than its sources" in str(x.message) for x in w)
