@@ -16,8 +16,8 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB_DIR = os.path.join(PKG, "lib")
 LIB = os.path.join(LIB_DIR, "libpaes_cuda.so")
-SOURCES = ["aes_kernels.cu", "runtime.cu", "abi_core.cu", "abi_batch.cu", "abi_file.cu", "host_rules.cpp"]
-HEADERS = ["aes_kernels.cuh", "aes_tables.hpp", "host_rules.hpp", "launch.hpp", "runtime.hpp", "sbox_bitsliced.inc",
+SOURCES = ["aes_kernels.cu", "runtime.cu", "abi_core.cu", "abi_batch.cu", "abi_file.cu", "host_rules.cpp", "host_copy.cpp"]
+HEADERS = ["aes_kernels.cuh", "aes_tables.hpp", "host_rules.hpp", "host_copy.hpp", "launch.hpp", "runtime.hpp", "sbox_bitsliced.inc",
            "gpu_worker.cpp"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

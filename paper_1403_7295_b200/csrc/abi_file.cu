@@ -21,6 +21,7 @@
 #include <string>
 #include <vector>
 
+#include "host_copy.hpp"
 #include "runtime.hpp"
 
 using namespace paes_b200;
@@ -178,7 +179,7 @@ std::uint64_t file_shard(DevCtx& d, const Range& r, int in_fd, int out_fd, std::
       // shared mapping proceed in parallel, and one pwrite per slot measured
       // slower on ext4 (1.22 vs 1.65 GB/s, 4 GiB)
       if (out_map)
-        par_io(len, io_threads, [&](std::uint64_t o, std::uint64_t n) { std::memcpy(out_map + base + o, slot + o, n); });
+        par_io(len, io_threads, [&](std::uint64_t o, std::uint64_t n) { bulk_copy(out_map + base + o, slot + o, n); });
       else
         par_io(len, io_threads, [&](std::uint64_t o, std::uint64_t n) { pwrite_all(out_fd, slot + o, n, base + o, out_path); });
     } catch (const IoFail& e) {

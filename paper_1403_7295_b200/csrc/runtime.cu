@@ -30,6 +30,7 @@
 #include <string>
 #include <thread>
 #include <vector>
+#include "host_copy.hpp"
 #include "runtime.hpp"
 
 namespace paes_b200::rt {
@@ -489,7 +490,7 @@ void CopyTeam::worker(unsigned idx, int dev) {
       b = std::min(n_, idx * step_);
       e = std::min(n_, (idx + 1) * step_);
     }
-    if (b < e) std::memcpy(dst + b, src + b, e - b);
+    if (b < e) bulk_copy(dst + b, src + b, e - b);
     {
       std::lock_guard<std::mutex> lk(mu_);
       if (--pending_ == 0) done_.notify_all();
@@ -516,7 +517,7 @@ void CopyTeam::copy(std::uint8_t* dst, const std::uint8_t* src, std::uint64_t n)
     ++gen_;
   }
   go_.notify_all();
-  std::memcpy(dst, src, std::min(n, step));
+  bulk_copy(dst, src, std::min(n, step));
   std::unique_lock<std::mutex> lk(mu_);
   done_.wait(lk, [&] { return pending_ == 0; });
 }
