@@ -48,9 +48,10 @@ static void worker(int id, int iters) {
     fill(data, rng);
     std::uint64_t m = 0, k = 0;
     switch (op) {
-      case 0: {  // pageable host chunk round trip
-        EXPECT(paes_cuda_chunk(0, data.data(), n, 1, rk, ct.data(), &m, 0) == 0, "pageable encrypt");
-        EXPECT(paes_cuda_chunk(1, ct.data(), m, 1, rk, back.data(), &k, 0) == 0, "pageable decrypt");
+      case 0: {  // pageable host chunk round trip; 3 explicit shards (the shard pool) or the auto rule
+        const int ng = (rng() % 2) ? 3 : 0;
+        EXPECT(paes_cuda_chunk(0, data.data(), n, 1, rk, ct.data(), &m, ng) == 0, "pageable encrypt");
+        EXPECT(paes_cuda_chunk(1, ct.data(), m, 1, rk, back.data(), &k, ng) == 0, "pageable decrypt");
         EXPECT(k == n && std::memcmp(back.data(), data.data(), n) == 0, "pageable round trip");
         break;
       }
