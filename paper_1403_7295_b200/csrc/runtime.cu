@@ -288,7 +288,10 @@ void ShardPool::loop(Worker* w) {
       bind_thread_to_device_numa(dev);
       bound = dev;
     }
-    job();
+    try {
+      job();
+    } catch (...) {  // callers wrap their work in guarded(); never let a pool thread die
+    }
     {
       std::lock_guard<std::mutex> lk(done_mu_);
       if (--pending_ == 0) done_cv_.notify_all();
