@@ -23,6 +23,7 @@
 #include <chrono>
 #include <condition_variable>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <mutex>
@@ -371,6 +372,34 @@ std::uint64_t pinned_piece_size(std::uint64_t len, std::uint64_t chunk) {
   return std::clamp<std::uint64_t>(p, 16, chunk);
 }
 
+// Piece lengths of the pinned ring over `len` bytes with nominal piece C.
+// The first copy-in and the last copy-out of a range run with nothing to
+// overlap them, so the ring ramps: C/8, C/4, C/2, C, ..., C, C/2, C/4, C/8
+// (every piece a multiple of 16 except the last, which takes the tail).
+// PAES_RING_RAMP=0 gives flat C pieces (A/B).
+std::vector<std::uint64_t> ring_pieces(std::uint64_t len, std::uint64_t C) {
+  static const bool ramp = [] {
+    const char* e = std::getenv("PAES_RING_RAMP");
+    return !(e && e[0] == '0');
+  }();
+  std::vector<std::uint64_t> p;
+  const std::uint64_t r1 = (C / 8) & ~std::uint64_t(15), r2 = (C / 4) & ~std::uint64_t(15),
+                      r3 = (C / 2) & ~std::uint64_t(15);
+  const std::uint64_t ramps = 2 * (r1 + r2 + r3);
+  if (!ramp || r1 == 0 || len < ramps + 2 * C) {
+    for (std::uint64_t off = 0; off < len || p.empty(); off += C) p.push_back(std::min(C, len - off));
+    return p;
+  }
+  p = {r1, r2, r3};
+  std::uint64_t mid = len - ramps;  // >= 2C
+  const std::uint64_t q = mid / C;
+  for (std::uint64_t i = 0; i < q; ++i) p.push_back(C);
+  mid -= q * C;
+  if (mid & ~std::uint64_t(15)) p.push_back(mid & ~std::uint64_t(15));
+  p.insert(p.end(), {r3, r2, r1 + (mid & 15)});
+  return p;
+}
+
 // Small host ranges (<= kSmallBytes): one memcpy into a mapped pinned buffer,
 // ONE kernel that reads and writes that host buffer over PCIe (zero-copy),
 // one sync, one memcpy out.  Replaces H2D + launch + D2H (three commands and
@@ -708,8 +737,8 @@ std::uint64_t run_host_range(DevCtx& d, const Range& r, const std::uint8_t* in, 
   if (!is_pinned(in) || !is_pinned(out)) return run_host_range_staged(d, r, in, out, kw);
   QuiesceOnThrow quiesce{d};
   const int S = static_cast<int>(d.st.size());
-  const std::uint64_t C = pinned_piece_size(r.in_len, d.chunk);
-  const std::uint64_t npieces = std::max<std::uint64_t>(1, (r.in_len + C - 1) / C);
+  const std::vector<std::uint64_t> pieces = ring_pieces(r.in_len, pinned_piece_size(r.in_len, d.chunk));
+  const std::uint64_t npieces = pieces.size();
   // the last piece's trailer check writes the mapped status word directly
   if (r.check_pad) *reinterpret_cast<volatile std::uint32_t*>(d.h_status) = 0xffffffffu;  // unchecked => PaddingError
   // One queue per engine: copy-in on st[0], kernels on st[1], copy-out on
@@ -721,11 +750,10 @@ std::uint64_t run_host_range(DevCtx& d, const Range& r, const std::uint8_t* in, 
   // (scripts/ring_overhead_probe.cu, 1 GiB, empty kernel: 43.3 -> 45.0 GB/s at
   // 8 MiB pieces, 46.2 -> 47.1 at 16 MiB).
   cudaStream_t sin = d.st[0], sk = d.st[1 % S], sout = d.st[2 % S];
-  std::uint64_t out_total = 0;
-  for (std::uint64_t k = 0; k < npieces; ++k) {
+  std::uint64_t out_total = 0, off = 0;
+  for (std::uint64_t k = 0; k < npieces; off += pieces[k], ++k) {
     const int s = static_cast<int>(k % S);
-    const std::uint64_t off = k * C;
-    const std::uint64_t len = std::min<std::uint64_t>(C, r.in_len - off);
+    const std::uint64_t len = pieces[k];
     const bool last = k + 1 == npieces;
     EcbArgs a = make_args(r, d.dbuf[s], d.dbuf[s], len, last, kw, d.m_status);
     if (k >= static_cast<std::uint64_t>(S)) PAES_CK(cudaStreamWaitEvent(sin, d.ev_out[s], 0));
