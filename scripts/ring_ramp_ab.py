@@ -1,6 +1,8 @@
 """E2E through paes_cuda_chunk on pinned buffers (the pinned ring) at the
-configs' sizes, for the ring's piece ramp A/B:
-    PAES_RING_RAMP=0|1 python scripts/ring_ramp_ab.py
+configs' sizes.  Round 2 used it for an A/B of a ramped piece schedule
+(C/8, C/4, C/2 at both ends, PAES_RING_RAMP=1 in that build): no gain, not
+adopted (profiles/r02_ring_ramp_ab.jsonl).
+    python scripts/ring_ramp_ab.py
 Prints one JSON line: median GB/s of 7 calls (after 2 warm) per size and direction."""
 import ctypes as C
 import json
