@@ -943,9 +943,13 @@ class ConfigBench:
                 "api": "paes.encrypt_bytes / decrypt_bytes (the _paes drop-in; library-staged pinned ring)",
                 "parity": "ok" if ok else "MISMATCH"}
 
-    # -- the paper's own metric: file -> file run_job, next to the reference's
+    # -- the paper's own metric: file -> file run_job, next to the reference's,
+    #    through the reference's own harness contract (measure_cell + CSV)
     def file_e2e(self):
         import oracle
+
+        from paper_1403_7295_b200 import build as B
+        from paper_1403_7295_b200 import report
 
         paes = self.paes
         host, e = self.big
@@ -960,37 +964,48 @@ class ConfigBench:
             key = paes.sweep(2, 16)
             R = oracle.RefLib()
             phys, logical = R.cores()
+            ngpu = paes.device_count()
 
-            def cell(fn):
+            def cell(fn, workers, strategy):
                 fn()  # warm: page cache, CUDA context, pinned ring
-                samples = [fn() for _ in range(3)]
-                kept = R.reject_outliers(samples)  # measure_cell (bench.cpp:81-107)
-                return sum(kept) / len(kept), samples
+                rec = report.measure_cell(fn, n, workers, strategy, 3, logical)  # bench.cpp:81-107
+                if rec.failed:
+                    raise RuntimeError(f"{strategy} cell failed: {rec.error}")
+                return rec
 
-            enc_s, enc_samples = cell(lambda: paes.encrypt_file(src, ct, key, workers=1, strategy="gpu")["seconds"])
-            ok = hashlib.sha256(open(ct, "rb").read()).hexdigest() == e["ct_sha256"]
-            dec_s, _ = cell(lambda: paes.decrypt_file(ct, pt, key, workers=1, strategy="gpu")["seconds"])
-            ok = ok and hashlib.sha256(open(pt, "rb").read()).hexdigest() == e["pt_sha256"]
-            os.unlink(pt)
-
-            def ref_job():
-                rc, _, _, sec = R.run_job(src, pt, key, logical, 1, 0)
-                assert rc == 0, rc
+            def ref_job(strategy, workers, out, exe=""):
+                rc, _, _, sec = R.run_job(src, out, key, workers, strategy, 0, exe)
+                if rc:
+                    raise RuntimeError(f"reference run_job rc={rc}")
                 return sec
 
-            ref_s, ref_samples = cell(ref_job)
+            gpu = cell(lambda: paes.encrypt_file(src, ct, key, workers=ngpu, strategy="gpu")["seconds"], ngpu, "gpu")
+            ok = hashlib.sha256(open(ct, "rb").read()).hexdigest() == e["ct_sha256"]
+            dec = cell(lambda: paes.decrypt_file(ct, pt, key, workers=ngpu, strategy="gpu")["seconds"], ngpu, "gpu")
+            ok = ok and hashlib.sha256(open(pt, "rb").read()).hexdigest() == e["pt_sha256"]
+            # the reference's own process strategy, unmodified, spawning the GPU
+            # worker (one process per GPU)
+            proc = cell(lambda: ref_job(2, ngpu, pt, B.WORKER), ngpu, "processes+gpu_worker")
             ok = ok and open(pt, "rb").read() == open(ct, "rb").read()
-            return {"workload": f"run_job encrypt/decrypt file -> file on {d}, config3's 4 GiB + 7 input "
-                                f"(JobOutcome.seconds, measure_cell: 1 warm + 3 reps, reject_outliers mean)",
-                    "value": round(n / enc_s / 1e9, 3), "unit": "GB/s", "mbps": round(n * 8 / enc_s / 1e6, 1),
-                    "decrypt_value": round(m / dec_s / 1e9, 3),
+            thr = cell(lambda: ref_job(1, logical, pt), logical, "threads")
+            ok = ok and open(pt, "rb").read() == open(ct, "rb").read()
+            recs = [thr, gpu, proc]
+            return {"workload": f"run_job encrypt file -> file on {d}, config3's 4 GiB + 7 input (JobOutcome.seconds; "
+                                f"measure_cell: 1 warm + 3 reps, reject_outliers mean)",
+                    "value": round(n / gpu.avg_seconds / 1e9, 3), "unit": "GB/s", "mbps": round(gpu.throughput_mbps, 1),
+                    "decrypt_value": round(m / dec.avg_seconds / 1e9, 3),
                     "api": "paes_cuda_run_job (strategy gpu: pread -> pinned ring -> GPU -> writer, temp + rename)",
-                    "seconds": [round(x, 4) for x in enc_samples],
-                    "cpu_baseline": {"value": round(n / ref_s / 1e9, 3), "unit": "GB/s", "cores": logical,
+                    "seconds": [round(x, 4) for x in gpu.samples],
+                    "process_strategy_gpu_worker": {
+                        "value": round(n / proc.avg_seconds / 1e9, 3), "unit": "GB/s",
+                        "api": "reference run_job(ProcessIsolated, workers = #GPUs) with worker_exe = lib/paes_gpu_worker",
+                        "seconds": [round(x, 4) for x in proc.samples]},
+                    "cpu_baseline": {"value": round(n / thr.avg_seconds / 1e9, 3), "unit": "GB/s", "cores": logical,
                                      "physical_cores": phys, "kind": "reference",
                                      "sample": f"reference run_job(threads, {logical} workers) on the same file",
-                                     "seconds": [round(x, 4) for x in ref_samples]},
-                    "parity": "ok (sha256 == reference digest; reference output identical)" if ok else "MISMATCH"}
+                                     "seconds": [round(x, 4) for x in thr.samples]},
+                    "report_csv": report.to_csv(recs).splitlines(),
+                    "parity": "ok (sha256 == reference digest; reference outputs identical)" if ok else "MISMATCH"}
         finally:
             for p in (src, ct, pt):
                 if os.path.exists(p):

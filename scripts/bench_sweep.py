@@ -63,8 +63,9 @@ def main():
         for w in workers_cpu:
             records.append(report.measure_cell(lambda: ref_run(w), size, w, "threads", args.reps, logical))
         ngpu = paes.device_count()
-        paes.encrypt_file(path, out, key, workers=ngpu)  # warm-up (context, pinned ring)
-        records.append(report.measure_cell(lambda: paes.encrypt_file(path, out, key, workers=ngpu)["seconds"],
+        paes.encrypt_file(path, out, key, workers=ngpu, strategy="gpu")  # warm-up (context, pinned ring)
+        records.append(report.measure_cell(lambda: paes.encrypt_file(path, out, key, workers=ngpu,
+                                                                     strategy="gpu")["seconds"],
                                            size, ngpu, "gpu", args.reps, logical))
         for p in (path, out):
             if os.path.exists(p):
