@@ -44,6 +44,7 @@ def build(force: bool = False, verbose: bool = False, defines=(), out_lib: str |
     defaults."""
     lib = out_lib or LIB
     if not force and out_lib is None and not _stale():
+        _build_aux(missing_only=True)
         return LIB
     lib_dir = os.path.dirname(lib)
     os.makedirs(lib_dir, exist_ok=True)
@@ -72,9 +73,15 @@ def build(force: bool = False, verbose: bool = False, defines=(), out_lib: str |
     for o in objs:
         os.unlink(o)
     if out_lib is None:
-        build_worker()
-        build_bitsliced_ab()
+        _build_aux()
     return lib
+
+
+def _build_aux(missing_only: bool = False) -> None:
+    """The executables and libraries built next to libpaes_cuda.so."""
+    for path, fn in ((WORKER, build_worker), (BITSLICED_AB, build_bitsliced_ab), (AES_ABI, build_aes_abi)):
+        if not missing_only or not os.path.exists(path):
+            fn()
 
 
 BITSLICED_AB = os.path.join(LIB_DIR, "libpaes_bitsliced_ab.so")
@@ -108,6 +115,24 @@ def build_worker() -> str:
         raise RuntimeError("worker build failed:\n%s%s" % (r.stdout, r.stderr))
     os.replace(WORKER + ".tmp", WORKER)
     return WORKER
+
+
+AES_ABI = os.path.join(LIB_DIR, "libpaes_aes_b200.so")
+
+
+def build_aes_abi() -> str:
+    """libpaes_aes_b200.so: the reference's aes.cpp entry points (aes.hpp
+    mangled C++ symbols) backed by libpaes_cuda.so -- the link-level drop-in
+    (csrc/aes_cxx_abi.cpp)."""
+    cxx = "/usr/bin/g++" if os.path.exists("/usr/bin/g++") else "g++"
+    cmd = [cxx, "-std=c++20", "-O2", "-fPIC", "-shared", "-Wall", "-Wextra", f"-I{os.path.join(ROOT, 'include')}",
+           os.path.join(CSRC, "aes_cxx_abi.cpp"), "-o", AES_ABI + ".tmp", f"-L{LIB_DIR}", "-lpaes_cuda",
+           "-Wl,-rpath,$ORIGIN"]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError("aes ABI library build failed:\n%s%s" % (r.stdout, r.stderr))
+    os.replace(AES_ABI + ".tmp", AES_ABI)
+    return AES_ABI
 
 
 if __name__ == "__main__":
