@@ -400,45 +400,6 @@ std::vector<std::uint64_t> ring_pieces(std::uint64_t len, std::uint64_t C) {
   return p;
 }
 
-// Small host ranges (<= kSmallBytes): one memcpy into a mapped pinned buffer,
-// ONE kernel that reads and writes that host buffer over PCIe (zero-copy),
-// one sync, one memcpy out.  Replaces H2D + launch + D2H (three commands and
-// their latencies) for the short messages of config 3 / encrypt_bytes.
-constexpr std::uint64_t kSmallBytes = 1ull << 20;
-
-struct SmallBuf {
-  std::uint8_t* host = nullptr;  // mapped pinned, kSmallBytes + 32
-  std::uint8_t* dev = nullptr;   // its device alias
-  std::uint32_t* status_host = nullptr;
-  std::uint32_t* status_dev = nullptr;
-};
-SmallBuf g_small[kMaxDev];
-
-std::uint64_t run_small(DevCtx& d, const Range& r, const std::uint8_t* in, std::uint8_t* out, const KeyWords& kw) {
-  SmallBuf& sb = g_small[d.id];
-  if (!sb.host) {
-    void* p = nullptr;
-    PAES_CK(cudaHostAlloc(&p, kSmallBytes + 4096, cudaHostAllocMapped | cudaHostAllocPortable));
-    sb.host = static_cast<std::uint8_t*>(p);
-    PAES_CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&sb.dev), p, 0));
-    sb.status_host = reinterpret_cast<std::uint32_t*>(sb.host + kSmallBytes + 2048);
-    sb.status_dev = reinterpret_cast<std::uint32_t*>(sb.dev + kSmallBytes + 2048);
-  }
-  if (r.in_len) std::memcpy(sb.host, in, r.in_len);
-  *sb.status_host = 0xffffffffu;  // sentinel: unchecked => PaddingError
-  EcbArgs a = make_args(r, sb.dev, sb.dev, r.in_len, true, kw, sb.status_dev);
-  PAES_CK(launch_ecb(r.dec, a, d.sm_count, d.st[0]));
-  PAES_CK(cudaStreamSynchronize(d.st[0]));
-  std::uint64_t olen = a.nblocks * 16;
-  if (olen) std::memcpy(out, sb.host, olen);
-  if (r.check_pad) {
-    const std::uint32_t k = *reinterpret_cast<volatile std::uint32_t*>(sb.status_host);
-    if (k == 0xffffffffu) throw PaddingError("unpad: invalid pad bytes");
-    olen -= k;
-  }
-  return olen;
-}
-
 // Device alias of a page-locked host pointer (under UVA every cudaHostAlloc'd
 // or registered buffer is device-accessible), or nullptr for pageable memory.
 const void* pinned_alias(const void* p) {
@@ -453,25 +414,139 @@ const void* pinned_alias(const void* p) {
 
 bool is_pinned(const void* p) { return pinned_alias(p) != nullptr; }
 
-// Pinned host ranges up to g_zero_copy_max: ONE kernel reads and writes the
-// caller's buffers over PCIe through their UVA aliases -- no device ring, no
-// copy-engine commands, no per-piece latencies.  Measured against the copy
-// ring (profiles/r01_zero_copy_probe.json): 3.4x at 1 MiB, ahead up to
-// ~256 MiB; beyond that the copy engines' larger PCIe requests win (46 vs
-// 40 GB/s at 1 GiB).
-std::uint64_t run_zero_copy(DevCtx& d, const Range& r, const void* din, void* dout, const KeyWords& kw) {
-  if (r.check_pad) *reinterpret_cast<volatile std::uint32_t*>(d.h_status) = 0xffffffffu;  // unchecked => PaddingError
-  EcbArgs a = make_args(r, static_cast<const std::uint8_t*>(din), static_cast<std::uint8_t*>(dout), r.in_len, true, kw,
-                        d.m_status);
-  PAES_CK(launch_ecb(r.dec, a, d.sm_count, d.st[0]));
-  PAES_CK(cudaStreamSynchronize(d.st[0]));
-  std::uint64_t olen = a.nblocks * 16;
-  if (r.check_pad) {
-    const std::uint32_t k = *reinterpret_cast<volatile std::uint32_t*>(d.h_status);
-    if (k == 0xffffffffu) throw PaddingError("unpad: invalid pad bytes");
-    olen -= k;
+// ------------------------------------------------------------ short calls
+// Short host ranges run as ONE kernel that reads and writes host memory over
+// PCIe (zero-copy) -- no device ring, no copy-engine commands:
+// - pinned caller buffers up to g_zero_copy_max: the kernel works on the
+//   caller's buffers through their UVA aliases.  Measured against the copy
+//   ring (profiles/r01_zero_copy_probe.json): 3.4x at 1 MiB, ahead up to
+//   ~256 MiB; beyond that the copy engines' larger PCIe requests win (46 vs
+//   40 GB/s at 1 GiB);
+// - pageable buffers up to kSmallBytes: one memcpy into a mapped pinned
+//   bounce buffer, the kernel in place on it, one memcpy out (replaces H2D +
+//   launch + D2H, three commands and their latencies, for config 3's short
+//   messages and encrypt_bytes).
+// Each call leases a LANE of the device -- a stream, a mapped status word and
+// (after the first pageable call) a bounce buffer of its own -- from a pool,
+// instead of taking d.mu: short calls from many host threads overlap their
+// launch, kernel and synchronisation latencies rather than queueing behind
+// one lock (scripts/concurrent_small_probe.cu).  Lanes are created on demand,
+// reused, and never freed, so the pool holds as many as the peak number of
+// concurrent short calls (a stream + 4 KiB mapped, + 1 MiB pinned once used
+// for pageable data, per lane).
+constexpr std::uint64_t kSmallBytes = 1ull << 20;
+
+struct Lane {
+  cudaStream_t st = nullptr;
+  std::uint32_t* status_host = nullptr;  // mapped pinned page
+  std::uint32_t* status_dev = nullptr;
+  std::uint8_t* bounce_host = nullptr;  // mapped pinned, kSmallBytes + 16, lazy
+  std::uint8_t* bounce_dev = nullptr;
+};
+
+struct LanePool {
+  std::mutex mu;
+  std::vector<Lane*> free;
+};
+LanePool g_lanes[kMaxDev];
+
+class LaneLease {
+ public:
+  explicit LaneLease(DevCtx& d) : pool_(g_lanes[d.id]) {
+    {
+      std::lock_guard<std::mutex> lk(pool_.mu);
+      if (!pool_.free.empty()) {
+        lane_ = pool_.free.back();
+        pool_.free.pop_back();
+        return;
+      }
+    }
+    auto* l = new Lane();
+    try {
+      PAES_CK(cudaStreamCreateWithFlags(&l->st, cudaStreamNonBlocking));
+      void* p = nullptr;
+      PAES_CK(cudaHostAlloc(&p, 4096, cudaHostAllocMapped | cudaHostAllocPortable));
+      l->status_host = static_cast<std::uint32_t*>(p);
+      PAES_CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&l->status_dev), p, 0));
+    } catch (...) {
+      if (l->status_host) cudaFreeHost(l->status_host);
+      if (l->st) cudaStreamDestroy(l->st);
+      delete l;
+      throw;
+    }
+    lane_ = l;
   }
-  return olen;
+  ~LaneLease() {
+    // a call that failed with work queued drains it before the lane is reused
+    if (std::uncaught_exceptions() > depth_) cudaStreamSynchronize(lane_->st);
+    std::lock_guard<std::mutex> lk(pool_.mu);
+    pool_.free.push_back(lane_);
+  }
+  LaneLease(const LaneLease&) = delete;
+  LaneLease& operator=(const LaneLease&) = delete;
+  Lane& operator*() const { return *lane_; }
+
+ private:
+  LanePool& pool_;
+  Lane* lane_ = nullptr;
+  int depth_ = std::uncaught_exceptions();
+};
+
+// One zero-copy launch on the lane's stream over host memory (device aliases
+// din/dout), synchronised; returns the bytes written.  A checked trailer's
+// verdict lands in the lane's mapped word (finish_check reads it).
+std::uint64_t lane_launch(DevCtx& d, Lane& l, const Range& r, const void* din, void* dout, const KeyWords& kw) {
+  if (r.check_pad) *reinterpret_cast<volatile std::uint32_t*>(l.status_host) = 0xffffffffu;  // unchecked => PaddingError
+  EcbArgs a = make_args(r, static_cast<const std::uint8_t*>(din), static_cast<std::uint8_t*>(dout), r.in_len, true,
+                        kw, l.status_dev);
+  PAES_CK(launch_ecb(r.dec, a, d.sm_count, l.st));
+  PAES_CK(cudaStreamSynchronize(l.st));
+  return a.nblocks * 16;
+}
+
+// Output length after the trailer check (decrypt, final): unpadded, or PaddingError.
+std::uint64_t finish_check(const Lane& l, const Range& r, std::uint64_t olen) {
+  if (!r.check_pad) return olen;
+  const std::uint32_t k = *reinterpret_cast<volatile std::uint32_t*>(l.status_host);
+  if (k == 0xffffffffu) throw PaddingError("unpad: invalid pad bytes");
+  return olen - k;
+}
+
+std::uint64_t configured_chunk() {
+  std::lock_guard<std::mutex> lk(g_cfg_mu);
+  return g_chunk;
+}
+
+// The short-call path for this range, if it has one (no d.mu; see above).
+// Returns false when the range belongs to a ring.
+bool run_short(DevCtx& d, const Range& r, const std::uint8_t* in, std::uint8_t* out, const KeyWords& kw,
+               std::uint64_t* produced) {
+  const void* din = nullptr;
+  const void* dout = nullptr;
+  if (r.in_len && r.in_len <= g_zero_copy_max.load(std::memory_order_relaxed)) {
+    din = pinned_alias(in);
+    dout = din ? pinned_alias(out) : nullptr;
+  }
+  const bool zero_copy = din && dout;
+  if (!zero_copy && r.in_len > std::min(kSmallBytes, configured_chunk())) return false;
+  DeviceGuard g(d.id);
+  LaneLease lease(d);
+  Lane& l = *lease;
+  if (zero_copy) {
+    *produced = finish_check(l, r, lane_launch(d, l, r, din, const_cast<void*>(dout), kw));
+    return true;
+  }
+  if (!l.bounce_host) {
+    void* p = nullptr;
+    PAES_CK(cudaHostAlloc(&p, kSmallBytes + 16, cudaHostAllocMapped | cudaHostAllocPortable));
+    l.bounce_host = static_cast<std::uint8_t*>(p);
+    PAES_CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&l.bounce_dev), p, 0));
+  }
+  if (r.in_len) std::memcpy(l.bounce_host, in, r.in_len);
+  const std::uint64_t olen = lane_launch(d, l, r, l.bounce_dev, l.bounce_dev, kw);
+  if (olen) std::memcpy(out, l.bounce_host, olen);  // every block, as decrypt_ecb writes the whole span
+  *produced = finish_check(l, r, olen);
+  return true;
 }
 
 cudaError_t copy_h2d_aligned(void* dev, const void* host, std::uint64_t n, cudaStream_t s) {
@@ -720,20 +795,12 @@ std::uint64_t run_host_range_staged(DevCtx& d, const Range& r, const std::uint8_
   return out_total;
 }
 
-// Host range on one device (d.mu held): pinned up to g_zero_copy_max ->
-// zero-copy kernel on the caller's buffers; small pageable -> zero-copy via
-// the mapped bounce buffer; pageable -> staged ring; large pinned -> direct
-// ring.  Returns the number of output bytes
+// Host range on one device beyond the short-call path (d.mu held): pageable
+// -> staged ring; pinned -> direct ring.  Returns the number of output bytes
 // (decrypt with trailer check: unpadded).
 std::uint64_t run_host_range(DevCtx& d, const Range& r, const std::uint8_t* in, std::uint8_t* out, const KeyWords& kw) {
   DeviceGuard g(d.id);
   ensure_pipeline(d, false);
-  if (r.in_len && r.in_len <= g_zero_copy_max.load(std::memory_order_relaxed)) {
-    const void* din = pinned_alias(in);
-    const void* dout = din ? pinned_alias(out) : nullptr;
-    if (din && dout) return run_zero_copy(d, r, din, const_cast<void*>(dout), kw);
-  }
-  if (r.in_len <= std::min(kSmallBytes, d.chunk)) return run_small(d, r, in, out, kw);
   if (!is_pinned(in) || !is_pinned(out)) return run_host_range_staged(d, r, in, out, kw);
   QuiesceOnThrow quiesce{d};
   const int S = static_cast<int>(d.st.size());
@@ -810,6 +877,7 @@ int host_transform(int dir, const std::uint8_t* in, std::uint64_t len, bool is_f
     r.check_pad = dec && is_final && c.is_final;
     codes[i] = guarded([&] {
       DevCtx& d = device(devs[i]);
+      if (run_short(d, r, in + c.offset, out + c.offset, kw, &produced[i])) return PAES_OK;  // no d.mu
       std::lock_guard<std::mutex> lk(d.mu);
       produced[i] = run_host_range(d, r, in + c.offset, out + c.offset, kw);
       return PAES_OK;

@@ -142,3 +142,62 @@ def test_concurrent_final_device_decrypts_keep_their_own_verdicts(paes, gpu, orc
 
     with ThreadPoolExecutor(12) as ex:
         assert all(ex.map(run, jobs))
+
+
+def test_short_calls_from_many_threads_share_lanes_exactly(paes, gpu, orc):
+    """Short host calls (pinned zero-copy up to the zero-copy limit, pageable
+    bounce up to 1 MiB) run on leased lanes without the device lock
+    (runtime.cu run_short): 16 threads x 40 calls of mixed sizes, pinned and
+    pageable, encrypt and final decrypt, 1 in 8 decrypts with a wrong key.
+    Every result is the oracle's, every wrong key is PaddingError, and no
+    thread sees another's verdict or bytes."""
+    import ctypes as C
+
+    import torch
+
+    from paper_1403_7295_b200 import _native as N
+
+    L = N.load()
+    sizes = [0, 5, 16, 4095, 4096, 65543, 1 << 20]
+
+    def worker(t):
+        rnd = random.Random(1000 + t)
+        hin = torch.empty((1 << 20) + 32, dtype=torch.uint8).pin_memory()
+        hout = torch.empty((1 << 20) + 32, dtype=torch.uint8).pin_memory()
+        for i in range(40):
+            n = rnd.choice(sizes)
+            key = os.urandom(16)
+            data = os.urandom(n)
+            want = orc.encrypt_chunk(data, True, key)
+            if rnd.random() < 0.5:  # pinned: zero-copy kernel on the caller's buffers
+                hin[:n] = torch.frombuffer(bytearray(data), dtype=torch.uint8) if n else hin[:0]
+                ol = C.c_uint64(0)
+                rc = L.paes_cuda_chunk(0, C.c_void_p(hin.data_ptr()), n, 1, paes.round_keys(key),
+                                       C.c_void_p(hout.data_ptr()), C.byref(ol), 1)
+                assert rc == 0 and ol.value == len(want)
+                ct = hout[:ol.value].numpy().tobytes()
+                assert ct == want, (t, i, n, "pinned enc")
+                hin[:len(ct)] = torch.frombuffer(bytearray(ct), dtype=torch.uint8)
+                bad = rnd.random() < 0.125
+                rc = L.paes_cuda_chunk(1, C.c_void_p(hin.data_ptr()), len(ct), 1,
+                                       paes.round_keys(bytes(16) if bad else key), C.c_void_p(hout.data_ptr()),
+                                       C.byref(ol), 1)
+                if bad:
+                    assert rc == N.EBADMSG or (rc == 0 and hout[:ol.value].numpy().tobytes() != data)
+                else:
+                    assert rc == 0 and hout[:ol.value].numpy().tobytes() == data, (t, i, n, "pinned dec")
+            else:  # pageable: the lane's bounce buffer
+                ct = paes.encrypt_bytes(data, key)
+                assert ct == want, (t, i, n, "pageable enc")
+                if rnd.random() < 0.125:
+                    try:
+                        out = paes.decrypt_bytes(ct, bytes(16))
+                        assert out != data
+                    except paes.PaddingError:
+                        pass
+                else:
+                    assert paes.decrypt_bytes(ct, key) == data, (t, i, n, "pageable dec")
+        return t
+
+    with ThreadPoolExecutor(16) as ex:
+        assert sorted(ex.map(worker, range(16))) == list(range(16))
