@@ -431,9 +431,9 @@ bool is_pinned(const void* p) { return pinned_alias(p) != nullptr; }
 // instead of taking d.mu: short calls from many host threads overlap their
 // launch, kernel and synchronisation latencies rather than queueing behind
 // one lock (scripts/concurrent_small_probe.cu).  Lanes are created on demand,
-// reused, and never freed, so the pool holds as many as the peak number of
-// concurrent short calls (a stream + 4 KiB mapped, + 1 MiB pinned once used
-// for pageable data, per lane).
+// reused, and never freed; the pool holds as many as the peak number of
+// concurrent short calls, at most kMaxLanes (a stream + 4 KiB mapped, + 1 MiB
+// pinned once used for pageable data, per lane).
 constexpr std::uint64_t kSmallBytes = 1ull << 20;
 
 struct Lane {
@@ -446,20 +446,28 @@ struct Lane {
 
 struct LanePool {
   std::mutex mu;
+  std::condition_variable cv;
   std::vector<Lane*> free;
+  int created = 0;
 };
 LanePool g_lanes[kMaxDev];
+// Lanes per device: beyond this many concurrent short calls, callers wait for
+// a lane (bounds the pool at 64 streams and 64 MiB of pinned bounce buffers;
+// the 16-thread probe uses 16).
+constexpr int kMaxLanes = 64;
 
 class LaneLease {
  public:
   explicit LaneLease(DevCtx& d) : pool_(g_lanes[d.id]) {
     {
-      std::lock_guard<std::mutex> lk(pool_.mu);
+      std::unique_lock<std::mutex> lk(pool_.mu);
+      pool_.cv.wait(lk, [this] { return !pool_.free.empty() || pool_.created < kMaxLanes; });
       if (!pool_.free.empty()) {
         lane_ = pool_.free.back();
         pool_.free.pop_back();
         return;
       }
+      ++pool_.created;  // reserved; released again if the lane cannot be built
     }
     auto* l = new Lane();
     try {
@@ -472,6 +480,11 @@ class LaneLease {
       if (l->status_host) cudaFreeHost(l->status_host);
       if (l->st) cudaStreamDestroy(l->st);
       delete l;
+      {
+        std::lock_guard<std::mutex> lk(pool_.mu);
+        --pool_.created;
+      }
+      pool_.cv.notify_one();
       throw;
     }
     lane_ = l;
@@ -479,8 +492,11 @@ class LaneLease {
   ~LaneLease() {
     // a call that failed with work queued drains it before the lane is reused
     if (std::uncaught_exceptions() > depth_) cudaStreamSynchronize(lane_->st);
-    std::lock_guard<std::mutex> lk(pool_.mu);
-    pool_.free.push_back(lane_);
+    {
+      std::lock_guard<std::mutex> lk(pool_.mu);
+      pool_.free.push_back(lane_);
+    }
+    pool_.cv.notify_one();
   }
   LaneLease(const LaneLease&) = delete;
   LaneLease& operator=(const LaneLease&) = delete;
