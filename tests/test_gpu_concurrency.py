@@ -201,3 +201,21 @@ def test_short_calls_from_many_threads_share_lanes_exactly(paes, gpu, orc):
 
     with ThreadPoolExecutor(16) as ex:
         assert sorted(ex.map(worker, range(16))) == list(range(16))
+
+
+def test_more_short_callers_than_lanes_wait_their_turn(paes, gpu, orc):
+    """96 threads at once against a pool capped at 64 lanes per device: the
+    extra callers wait for a lane instead of failing or deadlocking."""
+    key = bytes(range(16))
+    data = [os.urandom(4096 + i) for i in range(96)]
+
+    def run(i):
+        for _ in range(5):
+            ct = paes.encrypt_bytes(data[i], key)
+            assert paes.decrypt_bytes(ct, key) == data[i]
+        return ct
+
+    with ThreadPoolExecutor(96) as ex:
+        cts = list(ex.map(run, range(96)))
+    for i in (0, 47, 95):
+        assert cts[i] == orc.encrypt_chunk(data[i], True, key)
