@@ -364,6 +364,10 @@ def run_b200(args, dist: Dist):
 
     dev = 0 if os.environ.get("PAES_BENCH_SHARED_DEVICE") == "1" else dist.local
     torch.cuda.set_device(dev)
+    # dirty page-cache data left by an earlier job on the box (e.g. a test
+    # suite's files) is written back in the background for tens of seconds,
+    # competing with the timed host<->device copies; flush it first
+    os.sync()
     paes.set_devices([dev])
     numa = bind_to_gpu_numa(torch, dev) if dist.world > 1 else "unbound (N = 1: all host cores)"
     N = dist.world
@@ -1013,6 +1017,7 @@ class ConfigBench:
 
 
 def run_configs(args, torch, paes, dev, sms):
+    os.sync()  # no background writeback during the host-path legs (see run_b200)
     cb = ConfigBench(args, torch, paes, dev, sms)
     out = {}
     peaks, _ = measured_peaks()
