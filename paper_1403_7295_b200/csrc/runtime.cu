@@ -511,11 +511,26 @@ class LaneLease {
 // One zero-copy launch on the lane's stream over host memory (device aliases
 // din/dout), synchronised; returns the bytes written.  A checked trailer's
 // verdict lands in the lane's mapped word (finish_check reads it).
+// CTAs of a zero-copy launch.  Its rate is set by PCIe, not the SMs (32 SMs
+// cipher ~190 GB/s), and fewer CTAs issuing host reads overlap reads with
+// writes better: 4 MiB pinned 29.0 -> 34.1 GB/s, 16 MiB 36.6 -> 38.3, 48 MiB
+// 38.9 -> 39.5, 1 MiB 22.4 -> 23.8 against one CTA per SM (both pools of
+// runs in profiles/r02_zero_copy_grid_ab.txt).  It also leaves the other SMs
+// to concurrent calls on other lanes.  PAES_ZC_GRID overrides it (A/B).
+int zero_copy_grid(int sm_count) {
+  static const int g = [] {
+    const char* e = std::getenv("PAES_ZC_GRID");
+    const int v = e ? std::atoi(e) : 0;
+    return v > 0 ? v : 32;
+  }();
+  return std::min(g, sm_count);
+}
+
 std::uint64_t lane_launch(DevCtx& d, Lane& l, const Range& r, const void* din, void* dout, const KeyWords& kw) {
   if (r.check_pad) *reinterpret_cast<volatile std::uint32_t*>(l.status_host) = 0xffffffffu;  // unchecked => PaddingError
   EcbArgs a = make_args(r, static_cast<const std::uint8_t*>(din), static_cast<std::uint8_t*>(dout), r.in_len, true,
                         kw, l.status_dev);
-  PAES_CK(launch_ecb(r.dec, a, d.sm_count, l.st));
+  PAES_CK(launch_ecb(r.dec, a, zero_copy_grid(d.sm_count), l.st));
   PAES_CK(cudaStreamSynchronize(l.st));
   return a.nblocks * 16;
 }
