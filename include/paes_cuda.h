@@ -25,7 +25,7 @@
  * Threading: all entry points are safe to call concurrently from several host
  * threads (the reference calls encrypt_ecb from W threads at once,
  * exec.cpp:153-175).  Short host-pointer calls (pinned ranges up to the
- * zero-copy limit, pageable ones up to 1 MiB) each lease a stream and status
+ * zero-copy limit, pageable ones up to 4 MiB) each lease a stream and status
  * word of their own and run concurrently; longer host-pointer calls serialise
  * per device on an internal lock; device-pointer calls are asynchronous on the
  * caller's stream unless stated otherwise.

@@ -422,10 +422,13 @@ bool is_pinned(const void* p) { return pinned_alias(p) != nullptr; }
 //   ring (profiles/r01_zero_copy_probe.json): 3.4x at 1 MiB, ahead up to
 //   ~256 MiB; beyond that the copy engines' larger PCIe requests win (46 vs
 //   40 GB/s at 1 GiB);
-// - pageable buffers up to kSmallBytes: one memcpy into a mapped pinned
-//   bounce buffer, the kernel in place on it, one memcpy out (replaces H2D +
-//   launch + D2H, three commands and their latencies, for config 3's short
-//   messages and encrypt_bytes).
+// - pageable buffers up to kBounceMax: pieces of kBouncePiece copied into
+//   one of two mapped pinned bounce buffers, the kernel in place on it, copied
+//   out -- double-buffered, so piece k's kernel runs while the host copies
+//   piece k-1 out and piece k+1 in (replaces H2D + launch + D2H, three
+//   commands and their latencies, and the staged ring's two copy teams and
+//   drainer, whose fixed cost is ~300 us: encrypt_bytes of 1 MiB + 7 took
+//   300-420 us there, 512 KiB 77 us here; profiles/r02_pageable_small_ab.txt).
 // Each call leases a LANE of the device -- a stream, a mapped status word and
 // (after the first pageable call) a bounce buffer of its own -- from a pool,
 // instead of taking d.mu: short calls from many host threads overlap their
@@ -434,14 +437,16 @@ bool is_pinned(const void* p) { return pinned_alias(p) != nullptr; }
 // reused, and never freed; the pool holds as many as the peak number of
 // concurrent short calls, at most kMaxLanes (a stream + 4 KiB mapped, + 1 MiB
 // pinned once used for pageable data, per lane).
-constexpr std::uint64_t kSmallBytes = 1ull << 20;
+constexpr std::uint64_t kBouncePiece = 512ull << 10;  // a multiple of 16
+constexpr std::uint64_t kBounceMax = 4ull << 20;
 
 struct Lane {
   cudaStream_t st = nullptr;
   std::uint32_t* status_host = nullptr;  // mapped pinned page
   std::uint32_t* status_dev = nullptr;
-  std::uint8_t* bounce_host = nullptr;  // mapped pinned, kSmallBytes + 16, lazy
+  std::uint8_t* bounce_host = nullptr;  // mapped pinned, 2 x (kBouncePiece + 16), lazy
   std::uint8_t* bounce_dev = nullptr;
+  cudaEvent_t done[2] = {nullptr, nullptr};  // kernel on bounce half 0 / 1 finished
 };
 
 struct LanePool {
@@ -548,6 +553,52 @@ std::uint64_t configured_chunk() {
   return g_chunk;
 }
 
+// Pageable range through the lane's two bounce halves (see above).  Piece k's
+// kernel is queued before the host copies piece k-1 out, so kernel and host
+// copies overlap; half k%2 is refilled only after piece k-2 was copied out.
+// Every output block is copied out (decrypt_ecb writes the whole span), then
+// a checked trailer is settled.
+std::uint64_t run_bounce(DevCtx& d, Lane& l, const Range& r, const std::uint8_t* in, std::uint8_t* out,
+                         const KeyWords& kw) {
+  constexpr std::uint64_t kHalf = kBouncePiece + 16;
+  if (!l.bounce_host) {
+    void* p = nullptr;
+    PAES_CK(cudaHostAlloc(&p, 2 * kHalf, cudaHostAllocMapped | cudaHostAllocPortable));
+    l.bounce_host = static_cast<std::uint8_t*>(p);
+    PAES_CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&l.bounce_dev), p, 0));
+    for (auto& e : l.done) PAES_CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
+  if (r.check_pad) *reinterpret_cast<volatile std::uint32_t*>(l.status_host) = 0xffffffffu;  // unchecked => PaddingError
+  // balanced pieces of at most kBouncePiece (a 7-byte tail must not become a
+  // piece of its own with nothing to overlap)
+  const std::uint64_t want = std::max<std::uint64_t>(1, (r.in_len + kBouncePiece - 1) / kBouncePiece);
+  const std::uint64_t C =
+      std::clamp<std::uint64_t>(((r.in_len + want - 1) / want + 15) & ~std::uint64_t(15), 16, kBouncePiece);
+  const std::uint64_t npieces = std::max<std::uint64_t>(1, (r.in_len + C - 1) / C);
+  const int grid = zero_copy_grid(d.sm_count);
+  std::uint64_t prev_off = 0, prev_len = 0, total = 0;
+  for (std::uint64_t k = 0; k < npieces; ++k) {
+    const int h = static_cast<int>(k & 1);
+    const std::uint64_t off = k * C;
+    const std::uint64_t len = std::min(C, r.in_len - off);
+    if (len) std::memcpy(l.bounce_host + h * kHalf, in + off, len);
+    EcbArgs a = make_args(r, l.bounce_dev + h * kHalf, l.bounce_dev + h * kHalf, len, k + 1 == npieces, kw,
+                          l.status_dev);
+    PAES_CK(launch_ecb(r.dec, a, grid, l.st));
+    PAES_CK(cudaEventRecord(l.done[h], l.st));
+    if (k) {  // piece k-1, while piece k's kernel runs
+      PAES_CK(cudaEventSynchronize(l.done[h ^ 1]));
+      std::memcpy(out + prev_off, l.bounce_host + (h ^ 1) * kHalf, prev_len);
+    }
+    prev_off = off;
+    prev_len = a.nblocks * 16;
+    total = off + prev_len;
+  }
+  PAES_CK(cudaEventSynchronize(l.done[(npieces - 1) & 1]));
+  if (prev_len) std::memcpy(out + prev_off, l.bounce_host + ((npieces - 1) & 1) * kHalf, prev_len);
+  return finish_check(l, r, total);
+}
+
 // The short-call path for this range, if it has one (no d.mu; see above).
 // Returns false when the range belongs to a ring.
 bool run_short(DevCtx& d, const Range& r, const std::uint8_t* in, std::uint8_t* out, const KeyWords& kw,
@@ -559,7 +610,7 @@ bool run_short(DevCtx& d, const Range& r, const std::uint8_t* in, std::uint8_t* 
     dout = din ? pinned_alias(out) : nullptr;
   }
   const bool zero_copy = din && dout;
-  if (!zero_copy && r.in_len > std::min(kSmallBytes, configured_chunk())) return false;
+  if (!zero_copy && r.in_len > std::min(kBounceMax, configured_chunk())) return false;
   DeviceGuard g(d.id);
   LaneLease lease(d);
   Lane& l = *lease;
@@ -567,16 +618,7 @@ bool run_short(DevCtx& d, const Range& r, const std::uint8_t* in, std::uint8_t* 
     *produced = finish_check(l, r, lane_launch(d, l, r, din, const_cast<void*>(dout), kw));
     return true;
   }
-  if (!l.bounce_host) {
-    void* p = nullptr;
-    PAES_CK(cudaHostAlloc(&p, kSmallBytes + 16, cudaHostAllocMapped | cudaHostAllocPortable));
-    l.bounce_host = static_cast<std::uint8_t*>(p);
-    PAES_CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&l.bounce_dev), p, 0));
-  }
-  if (r.in_len) std::memcpy(l.bounce_host, in, r.in_len);
-  const std::uint64_t olen = lane_launch(d, l, r, l.bounce_dev, l.bounce_dev, kw);
-  if (olen) std::memcpy(out, l.bounce_host, olen);  // every block, as decrypt_ecb writes the whole span
-  *produced = finish_check(l, r, olen);
+  *produced = run_bounce(d, l, r, in, out, kw);
   return true;
 }
 

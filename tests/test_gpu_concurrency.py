@@ -146,7 +146,7 @@ def test_concurrent_final_device_decrypts_keep_their_own_verdicts(paes, gpu, orc
 
 def test_short_calls_from_many_threads_share_lanes_exactly(paes, gpu, orc):
     """Short host calls (pinned zero-copy up to the zero-copy limit, pageable
-    bounce up to 1 MiB) run on leased lanes without the device lock
+    bounce up to 4 MiB) run on leased lanes without the device lock
     (runtime.cu run_short): 16 threads x 40 calls of mixed sizes, pinned and
     pageable, encrypt and final decrypt, 1 in 8 decrypts with a wrong key.
     Every result is the oracle's, every wrong key is PaddingError, and no

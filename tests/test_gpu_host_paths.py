@@ -1,6 +1,6 @@
 """The host-pointer paths of paes_cuda_chunk, each forced explicitly: the
 zero-copy kernel on pinned buffers, the pinned direct ring (zero-copy off),
-the mapped bounce buffer for small pageable ranges and the staged ring for
+the double-buffered bounce path for pageable ranges up to 4 MiB and the staged ring for
 pageable memory -- all bit-exact vs the oracle across piece boundaries, and
 each rejecting a wrong key."""
 import ctypes as C
@@ -74,7 +74,7 @@ def test_oversized_pipeline_fails_cleanly_and_recovers(paes, gpu, orc):
     half-built ring behind, and the next call with a sane pipeline works."""
     rnd = random.Random(77)
     key = rnd.randbytes(16)
-    data = rnd.randbytes(3 * MiB + 5)  # pageable, > the 1 MiB bounce buffer: the staged ring
+    data = rnd.randbytes(5 * MiB + 5)  # pageable, > the 4 MiB bounce path: the staged ring
     try:
         paes.set_pipeline(16 << 30, 32)  # 32 x 16 GiB of device slots: cannot fit
         with pytest.raises(paes.GpuError):
@@ -131,7 +131,7 @@ def test_parallel_host_copies_cover_every_byte(paes, gpu, orc, tmp_path):
     (L = 6n + 75 gives 6 pieces of round16(n) .. n bytes, T = 2 parts)."""
     key = bytes(range(16))
     rnd = random.Random(4096)
-    for m in (40, 64, 100):
+    for m in (160, 200, 300):  # > the 4 MiB bounce path; 4 MiB pieces, then a last piece of that form too
         for r in (1, 5, 7):
             n = 8 * 4096 * m + r
             data = np.frombuffer(rnd.randbytes(n), dtype=np.uint8)
@@ -228,3 +228,36 @@ def test_short_calls_stay_on_one_listed_gpu(paes, gpu, orc):
             assert paes.decrypt_chunk(ct, True, key) == big
     finally:
         paes.set_devices([])
+
+
+def test_pageable_bounce_pieces(paes, gpu, orc):
+    """Pageable ranges up to 4 MiB go through a lane's two mapped bounce
+    halves in balanced pieces of at most 512 KiB (runtime.cu run_bounce):
+    piece edges, the 7-byte tail, exact aliasing and a wrong key, vs the oracle."""
+    rnd = random.Random(512)
+    key = rnd.randbytes(16)
+    bad = bytes([key[0] ^ 1]) + key[1:]
+    K = 512 * 1024
+    for n in (0, 15, 16, K - 1, K, K + 7, 2 * K - 16, 2 * K + 1, (1 << 20) + 7, 3 * MiB + 9, 4 * MiB - 16, 4 * MiB):
+        data = rnd.randbytes(n)
+        src = np.frombuffer(bytearray(data) + bytearray(32), dtype=np.uint8)
+        dst = np.zeros(n + 32, dtype=np.uint8)
+        want = orc.encrypt_chunk(data, True, key)
+        m = _run(paes, 0, src.ctypes.data, n, True, key, dst.ctypes.data)
+        assert m == len(want) and dst[:m].tobytes() == want, n
+        back = np.zeros(n + 32, dtype=np.uint8)
+        assert _run(paes, 1, dst.ctypes.data, m, True, key, back.ctypes.data) == n
+        assert back[:n].tobytes() == data, n
+        # in place (exact aliasing), both directions
+        buf = np.frombuffer(bytearray(want) + bytearray(16), dtype=np.uint8)
+        assert _run(paes, 1, buf.ctypes.data, m, True, key, buf.ctypes.data) == n
+        assert buf[:n].tobytes() == data, n
+        try:
+            expect = orc.decrypt_chunk(want, True, bad)
+        except ValueError:
+            expect = None
+        if expect is None:
+            _run(paes, 1, dst.ctypes.data, m, True, bad, back.ctypes.data, expect_rc=-74)
+        else:
+            k = _run(paes, 1, dst.ctypes.data, m, True, bad, back.ctypes.data)
+            assert back[:k].tobytes() == expect
