@@ -513,9 +513,6 @@ class LaneLease {
   int depth_ = std::uncaught_exceptions();
 };
 
-// One zero-copy launch on the lane's stream over host memory (device aliases
-// din/dout), synchronised; returns the bytes written.  A checked trailer's
-// verdict lands in the lane's mapped word (finish_check reads it).
 // CTAs of a zero-copy launch.  Its rate is set by PCIe, not the SMs (32 SMs
 // cipher ~190 GB/s), and fewer CTAs issuing host reads overlap reads with
 // writes better: 4 MiB pinned 29.0 -> 34.1 GB/s, 16 MiB 36.6 -> 38.3, 48 MiB
@@ -531,6 +528,9 @@ int zero_copy_grid(int sm_count) {
   return std::min(g, sm_count);
 }
 
+// One zero-copy launch on the lane's stream over host memory (device aliases
+// din/dout), synchronised; returns the bytes written.  A checked trailer's
+// verdict lands in the lane's mapped word (finish_check reads it).
 std::uint64_t lane_launch(DevCtx& d, Lane& l, const Range& r, const void* din, void* dout, const KeyWords& kw) {
   if (r.check_pad) *reinterpret_cast<volatile std::uint32_t*>(l.status_host) = 0xffffffffu;  // unchecked => PaddingError
   EcbArgs a = make_args(r, static_cast<const std::uint8_t*>(din), static_cast<std::uint8_t*>(dout), r.in_len, true,
@@ -561,12 +561,24 @@ std::uint64_t configured_chunk() {
 std::uint64_t run_bounce(DevCtx& d, Lane& l, const Range& r, const std::uint8_t* in, std::uint8_t* out,
                          const KeyWords& kw) {
   constexpr std::uint64_t kHalf = kBouncePiece + 16;
-  if (!l.bounce_host) {
+  if (!l.bounce_host) {  // all or nothing: a half-built bounce must not be reused
     void* p = nullptr;
-    PAES_CK(cudaHostAlloc(&p, 2 * kHalf, cudaHostAllocMapped | cudaHostAllocPortable));
+    std::uint8_t* dp = nullptr;
+    cudaEvent_t ev[2] = {nullptr, nullptr};
+    try {
+      PAES_CK(cudaHostAlloc(&p, 2 * kHalf, cudaHostAllocMapped | cudaHostAllocPortable));
+      PAES_CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&dp), p, 0));
+      for (auto& e : ev) PAES_CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    } catch (...) {
+      for (auto e : ev)
+        if (e) cudaEventDestroy(e);
+      if (p) cudaFreeHost(p);
+      throw;
+    }
     l.bounce_host = static_cast<std::uint8_t*>(p);
-    PAES_CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&l.bounce_dev), p, 0));
-    for (auto& e : l.done) PAES_CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    l.bounce_dev = dp;
+    l.done[0] = ev[0];
+    l.done[1] = ev[1];
   }
   if (r.check_pad) *reinterpret_cast<volatile std::uint32_t*>(l.status_host) = 0xffffffffu;  // unchecked => PaddingError
   // balanced pieces of at most kBouncePiece (a 7-byte tail must not become a
