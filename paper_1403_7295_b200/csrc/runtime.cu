@@ -729,8 +729,12 @@ constexpr std::uint64_t kStagedSlot = 64ull << 20;
 #ifndef PAES_STAGED_DIV
 #define PAES_STAGED_DIV 8
 #endif
+#ifndef PAES_STAGED_MIN_KIB
+#define PAES_STAGED_MIN_KIB 4096
+#endif
 std::uint64_t staged_piece_size(std::uint64_t len, std::uint64_t chunk) {
-  const std::uint64_t p = std::clamp<std::uint64_t>(len / PAES_STAGED_DIV, 4ull << 20, kStagedSlot);
+  const std::uint64_t p =
+      std::clamp<std::uint64_t>(len / PAES_STAGED_DIV, std::uint64_t(PAES_STAGED_MIN_KIB) << 10, kStagedSlot);
   return std::min((p + 15) & ~std::uint64_t(15), chunk);  // chunk: the device slot (a multiple of 16)
 }
 

@@ -1,7 +1,7 @@
 """Pageable (Python bytes) encrypt_bytes / decrypt_bytes at 16 KiB .. 8 MiB,
 single thread, best of R: GB/s and us per call.  Run with PAES_BOUNCE_MAX=0
 to push every size onto the staged ring (A/B of the bounce-buffer path).
-    python scripts/pageable_small_probe.py [reps=30]"""
+    python scripts/pageable_small_probe.py [reps=30] [sizes_kib=16,64,256,512,1024,2048,8192]"""
 import json
 import os
 import sys
@@ -13,7 +13,8 @@ from paper_1403_7295_b200 import paes  # noqa: E402
 reps = int(sys.argv[1]) if len(sys.argv) > 1 else 30
 key = bytes(range(16))
 res = {}
-for kib in (16, 64, 256, 512, 1024, 2048, 8192):
+sizes = [int(x) for x in (sys.argv[2] if len(sys.argv) > 2 else "16,64,256,512,1024,2048,8192").split(",")]
+for kib in sizes:
     n = kib * 1024 + 7
     data = os.urandom(n)
     ct = paes.encrypt_bytes(data, key)
