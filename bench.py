@@ -311,12 +311,22 @@ def run_reference(args, rank: int):
 
 
 def cpu_baseline(args):
-    R, key, pt, ct, workers, phys = reference_sample(args.total_bytes, args.seed, target_s=4.0)  # ~10-20 s of CPU work over 5 reps
-    samples = []
-    for _ in range(5):
-        t = time.perf_counter()
-        R.threads_into(0, pt.ctypes.data, pt.nbytes, key, ct.ctypes.data, workers)
-        samples.append(time.perf_counter() - t)
+    # every host core, even when this rank was bound to its GPU's NUMA node
+    # (N > 1): the baseline runs after all timed regions
+    bound = os.sched_getaffinity(0)
+    try:
+        os.sched_setaffinity(0, range(os.cpu_count() or 1))
+    except OSError:
+        pass
+    try:
+        R, key, pt, ct, workers, phys = reference_sample(args.total_bytes, args.seed, target_s=4.0)  # ~10-20 s over 5 reps
+        samples = []
+        for _ in range(5):
+            t = time.perf_counter()
+            R.threads_into(0, pt.ctypes.data, pt.nbytes, key, ct.ctypes.data, workers)
+            samples.append(time.perf_counter() - t)
+    finally:
+        os.sched_setaffinity(0, bound)
     kept = R.reject_outliers(samples)  # the reference's own method (bench.cpp:49-79)
     avg = sum(kept) / len(kept)
     return {"value": round(pt.nbytes / avg / 1e9, 4), "unit": "GB/s", "cores": workers, "physical_cores": phys,
