@@ -400,19 +400,32 @@ std::vector<std::uint64_t> ring_pieces(std::uint64_t len, std::uint64_t C) {
   return p;
 }
 
-// Device alias of a page-locked host pointer (under UVA every cudaHostAlloc'd
-// or registered buffer is device-accessible), or nullptr for pageable memory.
-const void* pinned_alias(const void* p) {
-  if (!p) return nullptr;
+// What a host-pointer entry was handed.  Page-locked host memory (under UVA
+// every cudaHostAlloc'd or registered buffer is device-accessible) carries
+// its device alias; pageable and managed memory are copied by the host; a
+// device pointer is the caller's mistake (the device-pointer entries take
+// those) and is rejected before the host could dereference it.
+struct HostPtr {
+  const std::uint8_t* alias = nullptr;  // device alias of the buffer's start, or nullptr
+  std::uint8_t* at(std::uint64_t off) const {
+    return alias ? const_cast<std::uint8_t*>(alias) + off : nullptr;
+  }
+};
+
+HostPtr classify_host(const void* p, const char* what) {
+  HostPtr h;
+  if (!p) return h;
   cudaPointerAttributes a{};
   if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
     cudaGetLastError();
-    return nullptr;
+    return h;
   }
-  return a.type == cudaMemoryTypeHost ? a.devicePointer : nullptr;
+  if (a.type == cudaMemoryTypeDevice)
+    throw std::invalid_argument(std::string(what) + " is device memory: host-pointer entries take host buffers "
+                                "(use the *_device entry points for device buffers)");
+  if (a.type == cudaMemoryTypeHost) h.alias = static_cast<const std::uint8_t*>(a.devicePointer);
+  return h;
 }
-
-bool is_pinned(const void* p) { return pinned_alias(p) != nullptr; }
 
 // ------------------------------------------------------------ short calls
 // Short host ranges run as ONE kernel that reads and writes host memory over
@@ -613,21 +626,15 @@ std::uint64_t run_bounce(DevCtx& d, Lane& l, const Range& r, const std::uint8_t*
 
 // The short-call path for this range, if it has one (no d.mu; see above).
 // Returns false when the range belongs to a ring.
-bool run_short(DevCtx& d, const Range& r, const std::uint8_t* in, std::uint8_t* out, const KeyWords& kw,
-               std::uint64_t* produced) {
-  const void* din = nullptr;
-  const void* dout = nullptr;
-  if (r.in_len && r.in_len <= g_zero_copy_max.load(std::memory_order_relaxed)) {
-    din = pinned_alias(in);
-    dout = din ? pinned_alias(out) : nullptr;
-  }
-  const bool zero_copy = din && dout;
+bool run_short(DevCtx& d, const Range& r, const std::uint8_t* in, std::uint8_t* out, const void* din, void* dout,
+               const KeyWords& kw, std::uint64_t* produced) {
+  const bool zero_copy = din && dout && r.in_len && r.in_len <= g_zero_copy_max.load(std::memory_order_relaxed);
   if (!zero_copy && r.in_len > std::min(kBounceMax, configured_chunk())) return false;
   DeviceGuard g(d.id);
   LaneLease lease(d);
   Lane& l = *lease;
   if (zero_copy) {
-    *produced = finish_check(l, r, lane_launch(d, l, r, din, const_cast<void*>(dout), kw));
+    *produced = finish_check(l, r, lane_launch(d, l, r, din, dout, kw));
     return true;
   }
   *produced = run_bounce(d, l, r, in, out, kw);
@@ -885,12 +892,13 @@ std::uint64_t run_host_range_staged(DevCtx& d, const Range& r, const std::uint8_
 }
 
 // Host range on one device beyond the short-call path (d.mu held): pageable
-// -> staged ring; pinned -> direct ring.  Returns the number of output bytes
-// (decrypt with trailer check: unpadded).
-std::uint64_t run_host_range(DevCtx& d, const Range& r, const std::uint8_t* in, std::uint8_t* out, const KeyWords& kw) {
+// -> staged ring; pinned (both buffers) -> direct ring.  Returns the number of
+// output bytes (decrypt with trailer check: unpadded).
+std::uint64_t run_host_range(DevCtx& d, const Range& r, const std::uint8_t* in, std::uint8_t* out, bool pinned,
+                             const KeyWords& kw) {
   DeviceGuard g(d.id);
   ensure_pipeline(d, false);
-  if (!is_pinned(in) || !is_pinned(out)) return run_host_range_staged(d, r, in, out, kw);
+  if (!pinned) return run_host_range_staged(d, r, in, out, kw);
   QuiesceOnThrow quiesce{d};
   const int S = static_cast<int>(d.st.size());
   const std::vector<std::uint64_t> pieces = ring_pieces(r.in_len, pinned_piece_size(r.in_len, d.chunk));
@@ -950,6 +958,7 @@ int host_transform(int dir, const std::uint8_t* in, std::uint64_t len, bool is_f
   }
   if (!out) throw std::invalid_argument("null output");
   check_alias(in, len, out, (is_final && !dec) ? (len / 16 + 1) * 16 : len);
+  const HostPtr hin = classify_host(in, "input"), hout = classify_host(out, "output");
   const auto devs = shard_devices(ngpus, len);
   const KeyWords kw = dec ? dec_key_words(rk) : enc_key_words(rk);
   const auto plan = dec ? plan_decrypt_chunks(len, static_cast<unsigned>(devs.size()))
@@ -966,9 +975,10 @@ int host_transform(int dir, const std::uint8_t* in, std::uint64_t len, bool is_f
     r.check_pad = dec && is_final && c.is_final;
     codes[i] = guarded([&] {
       DevCtx& d = device(devs[i]);
-      if (run_short(d, r, in + c.offset, out + c.offset, kw, &produced[i])) return PAES_OK;  // no d.mu
+      if (run_short(d, r, in + c.offset, out + c.offset, hin.at(c.offset), hout.at(c.offset), kw, &produced[i]))
+        return PAES_OK;  // no d.mu
       std::lock_guard<std::mutex> lk(d.mu);
-      produced[i] = run_host_range(d, r, in + c.offset, out + c.offset, kw);
+      produced[i] = run_host_range(d, r, in + c.offset, out + c.offset, hin.alias && hout.alias, kw);
       return PAES_OK;
     });
     if (codes[i]) msgs[i] = t_err;

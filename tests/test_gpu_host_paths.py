@@ -261,3 +261,24 @@ def test_pageable_bounce_pieces(paes, gpu, orc):
         else:
             k = _run(paes, 1, dst.ctypes.data, m, True, bad, back.ctypes.data)
             assert back[:k].tobytes() == expect
+
+
+def test_device_pointer_to_a_host_entry_is_einval(paes, gpu):
+    """A device buffer handed to a host-pointer entry is rejected up front
+    (EINVAL, naming the buffer) instead of being dereferenced by the host."""
+    import torch
+
+    from paper_1403_7295_b200 import _native as N
+
+    key = bytes(range(16))
+    d = torch.zeros(1 << 20, dtype=torch.uint8, device="cuda")
+    h = np.zeros((1 << 20) + 16, dtype=np.uint8)
+    L = N.load()
+    olen = C.c_uint64()
+    for src, dst, which in ((d.data_ptr(), h.ctypes.data, "input"), (h.ctypes.data, d.data_ptr(), "output")):
+        for n in (4096, 8 << 20):  # the lane path and the ring path
+            rc = L.paes_cuda_chunk(0, src, n, 1, paes.round_keys(key), dst, C.byref(olen), 1)
+            assert rc == N.EINVAL and which in N.last_error() and "device memory" in N.last_error()
+    # the library still works afterwards
+    data = os.urandom(5000)
+    assert paes.decrypt_bytes(paes.encrypt_bytes(data, key), key) == data
