@@ -35,6 +35,9 @@ MODULES = {
     "linked": os.path.join(ROOT, "oracle", "_ref", "linked"),
 }
 HOST_ONLY = "test_key_schedule_shape or test_plan_chunks or test_reject_outliers"
+# the library the reference modules link (their rpath), whatever PAES_CUDA_LIB
+# points this process at (e.g. the coverage variant)
+LINKED_LIB = os.path.join(ROOT, "paper_1403_7295_b200", "lib", "libpaes_cuda.so")
 
 
 def _staged():
@@ -102,11 +105,9 @@ print(json.dumps({"launches": lib.paes_cuda_launch_count() - before, "bad": bad,
 open(sys.argv[2], "wb").write(data + ct)
 """
     _staged()
-    from paper_1403_7295_b200 import _native
-
     blob = tmp_path / "blob.bin"
     env = dict(os.environ, PYTHONPATH=MODULES[which])
-    r = subprocess.run([sys.executable, "-c", snippet, os.path.realpath(_native.lib_path()), str(blob)], env=env,
+    r = subprocess.run([sys.executable, "-c", snippet, os.path.realpath(LINKED_LIB), str(blob)], env=env,
                        capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stdout + r.stderr
     import json
@@ -148,15 +149,13 @@ except (ValueError, RuntimeError) as e:  # PaddingError / WorkerError
 print(json.dumps({"launches": lib.paes_cuda_launch_count() - before, "enc": a, "dec": b, "bad": bad}))
 """
     _staged()
-    from paper_1403_7295_b200 import _native
-
     n = (5 << 20) + 7
     data = os.urandom(n)
     src, enc, dec = tmp_path / "in.bin", tmp_path / "in.enc", tmp_path / "in.dec"
     src.write_bytes(data)
     exe = os.path.join(ROOT, "paper_1403_7295_b200", "lib", "paes_gpu_worker") if strategy == "processes" else ""
     env = dict(os.environ, PYTHONPATH=MODULES["linked"])
-    r = subprocess.run([sys.executable, "-c", snippet, os.path.realpath(_native.lib_path()), str(src), str(enc),
+    r = subprocess.run([sys.executable, "-c", snippet, os.path.realpath(LINKED_LIB), str(src), str(enc),
                         str(dec), strategy, str(workers), exe], env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout + r.stderr
     import json
