@@ -377,6 +377,20 @@ __global__ void __launch_bounds__(kThreads, 1) ecb_kernel(const __grid_constant_
       }
     }
   }
+  if (a.done_flag) {  // uniform: the host spins on *done_flag (EcbArgs)
+    // the CTA's writes, ordered before thread 0's system-scope fence by the
+    // barrier (fences are cumulative: the cooperative-groups grid barrier
+    // pattern), then the count; one fence per CTA, not one per thread
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence_system();
+      if (atomicAdd(a.done_ctr, 1u) == gridDim.x - 1) {
+        *a.done_ctr = 0;  // ready for the next launch on the caller's stream (stream-ordered)
+        __threadfence_system();
+        *reinterpret_cast<volatile unsigned*>(a.done_flag) = a.done_seq;
+      }
+    }
+  }
 }
 
 // ---------------------------------------------------------------- batch

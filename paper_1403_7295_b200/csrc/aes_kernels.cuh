@@ -80,6 +80,14 @@ struct EcbArgs {
   // trailer) or ~0 for a malformed trailer -- the asynchronous face of
   // decrypt_chunk_into's unpad_final (exec.cpp:122-127)
   unsigned long long* result;
+  // optional completion signal for a host that spins instead of
+  // synchronising the stream (short host calls, runtime.cu lane_launch): after
+  // a barrier, each CTA's thread 0 fences to system scope, the CTAs count themselves in
+  // *done_ctr (device memory, 0 on entry; the last CTA resets it), and the
+  // last one writes done_seq to the mapped host word *done_flag
+  unsigned* done_ctr;
+  unsigned* done_flag;
+  unsigned done_seq;
   KeyWords k;
 };
 

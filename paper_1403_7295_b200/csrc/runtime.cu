@@ -455,8 +455,10 @@ constexpr std::uint64_t kBounceMax = 4ull << 20;
 
 struct Lane {
   cudaStream_t st = nullptr;
-  std::uint32_t* status_host = nullptr;  // mapped pinned page
+  std::uint32_t* status_host = nullptr;  // mapped pinned page: word 0 trailer status, word 16 completion flag
   std::uint32_t* status_dev = nullptr;
+  unsigned* ctr = nullptr;  // device word: CTAs of the lane's current kernel that have finished (EcbArgs::done_ctr)
+  unsigned seq = 0;         // last completion value handed to a kernel
   std::uint8_t* bounce_host = nullptr;  // mapped pinned, 2 x (kBouncePiece + 16), lazy
   std::uint8_t* bounce_dev = nullptr;
   cudaEvent_t done[2] = {nullptr, nullptr};  // kernel on bounce half 0 / 1 finished
@@ -494,7 +496,11 @@ class LaneLease {
       PAES_CK(cudaHostAlloc(&p, 4096, cudaHostAllocMapped | cudaHostAllocPortable));
       l->status_host = static_cast<std::uint32_t*>(p);
       PAES_CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&l->status_dev), p, 0));
+      l->status_host[16] = 0;
+      PAES_CK(cudaMalloc(reinterpret_cast<void**>(&l->ctr), sizeof(unsigned)));
+      PAES_CK(cudaMemset(l->ctr, 0, sizeof(unsigned)));
     } catch (...) {
+      if (l->ctr) cudaFree(l->ctr);
       if (l->status_host) cudaFreeHost(l->status_host);
       if (l->st) cudaStreamDestroy(l->st);
       delete l;
@@ -544,12 +550,60 @@ int zero_copy_grid(int sm_count) {
 // One zero-copy launch on the lane's stream over host memory (device aliases
 // din/dout), synchronised; returns the bytes written.  A checked trailer's
 // verdict lands in the lane's mapped word (finish_check reads it).
+// Completion of a lane's kernels.  The kernel's last CTA writes a sequence
+// number into the lane's mapped page after fencing every thread's writes to
+// system scope (EcbArgs::done_flag); the host spins on that word instead of
+// synchronising the stream, which skips the grid-completion semaphore round
+// trip: launch + completion of a one-CTA kernel 12.6 -> 9.3 us, 32 CTAs 16.0
+// -> 12.6-13.2 (scripts/sync_latency_probe.cu, profiles/r02_sync_latency.json).
+// The spin polls the stream every 1024 rounds, so a failed kernel surfaces its
+// error instead of hanging.  PAES_LANE_FLAG=0 synchronises the stream (A/B).
+bool lane_flags_on() {
+  static const bool on = [] {
+    const char* e = std::getenv("PAES_LANE_FLAG");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
+void arm_completion(Lane& l, EcbArgs& a) {
+  if (!lane_flags_on()) return;
+  a.done_ctr = l.ctr;
+  a.done_flag = l.status_dev + 16;
+  a.done_seq = ++l.seq;
+}
+
+// Waits until the lane's kernel that carries `seq` has finished (its writes
+// are visible to the host); earlier kernels on the lane finished before it.
+void wait_completion(Lane& l, unsigned seq) {
+  if (!lane_flags_on()) {
+    PAES_CK(cudaStreamSynchronize(l.st));
+    return;
+  }
+  const volatile unsigned* flag = l.status_host + 16;
+  for (unsigned spin = 1;; ++spin) {
+    if (static_cast<int>(*flag - seq) >= 0) break;
+    if ((spin & 1023) == 0) {
+      const cudaError_t e = cudaStreamQuery(l.st);
+      if (e == cudaErrorNotReady) continue;
+      if (e != cudaSuccess) {
+        cudaGetLastError();
+        throw CudaFail{PAES_ECUDA, std::string("lane kernel: ") + cudaGetErrorString(e)};
+      }
+      if (static_cast<int>(*flag - seq) >= 0) break;  // finished: the flag is visible now
+      throw CudaFail{PAES_ECUDA, "lane kernel finished without its completion flag"};
+    }
+  }
+  std::atomic_thread_fence(std::memory_order_acquire);  // host reads of the output after the flag
+}
+
 std::uint64_t lane_launch(DevCtx& d, Lane& l, const Range& r, const void* din, void* dout, const KeyWords& kw) {
   if (r.check_pad) *reinterpret_cast<volatile std::uint32_t*>(l.status_host) = 0xffffffffu;  // unchecked => PaddingError
   EcbArgs a = make_args(r, static_cast<const std::uint8_t*>(din), static_cast<std::uint8_t*>(dout), r.in_len, true,
                         kw, l.status_dev);
+  arm_completion(l, a);
   PAES_CK(launch_ecb(r.dec, a, zero_copy_grid(d.sm_count), l.st));
-  PAES_CK(cudaStreamSynchronize(l.st));
+  wait_completion(l, a.done_seq);
   return a.nblocks * 16;
 }
 
@@ -602,6 +656,7 @@ std::uint64_t run_bounce(DevCtx& d, Lane& l, const Range& r, const std::uint8_t*
   const std::uint64_t npieces = std::max<std::uint64_t>(1, (r.in_len + C - 1) / C);
   const int grid = zero_copy_grid(d.sm_count);
   std::uint64_t prev_off = 0, prev_len = 0, total = 0;
+  unsigned prev_seq = 0;
   for (std::uint64_t k = 0; k < npieces; ++k) {
     const int h = static_cast<int>(k & 1);
     const std::uint64_t off = k * C;
@@ -609,17 +664,21 @@ std::uint64_t run_bounce(DevCtx& d, Lane& l, const Range& r, const std::uint8_t*
     if (len) std::memcpy(l.bounce_host + h * kHalf, in + off, len);
     EcbArgs a = make_args(r, l.bounce_dev + h * kHalf, l.bounce_dev + h * kHalf, len, k + 1 == npieces, kw,
                           l.status_dev);
+    arm_completion(l, a);
     PAES_CK(launch_ecb(r.dec, a, grid, l.st));
-    PAES_CK(cudaEventRecord(l.done[h], l.st));
+    if (!lane_flags_on()) PAES_CK(cudaEventRecord(l.done[h], l.st));
     if (k) {  // piece k-1, while piece k's kernel runs
-      PAES_CK(cudaEventSynchronize(l.done[h ^ 1]));
+      if (lane_flags_on()) wait_completion(l, prev_seq);
+      else PAES_CK(cudaEventSynchronize(l.done[h ^ 1]));
       std::memcpy(out + prev_off, l.bounce_host + (h ^ 1) * kHalf, prev_len);
     }
     prev_off = off;
     prev_len = a.nblocks * 16;
+    prev_seq = a.done_seq;
     total = off + prev_len;
   }
-  PAES_CK(cudaEventSynchronize(l.done[(npieces - 1) & 1]));
+  if (lane_flags_on()) wait_completion(l, prev_seq);
+  else PAES_CK(cudaEventSynchronize(l.done[(npieces - 1) & 1]));
   if (prev_len) std::memcpy(out + prev_off, l.bounce_host + ((npieces - 1) & 1) * kHalf, prev_len);
   return finish_check(l, r, total);
 }
