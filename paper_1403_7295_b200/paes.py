@@ -184,16 +184,21 @@ def decrypt_block(block: bytes, key: bytes) -> bytes:
 
 
 # ---------------------------------------------------------------- chunks
+_TRIM_COPY_MAX = 256 * 1024  # a host copy of this many bytes costs about one short GPU call
+
+
 def chunk(direction: int, data, is_final: bool, key: bytes, ngpus: int = 0) -> bytes:
     """encrypt_chunk / decrypt_chunk (exec.hpp:61-65) over host memory."""
     rk = round_keys(key)
     src = _InBuf(data)
     L = N.load()
-    if direction == DECRYPT and is_final and src.n >= BLOCK and src.n % BLOCK == 0:
+    if direction == DECRYPT and is_final and src.n > _TRIM_COPY_MAX and src.n % BLOCK == 0:
         # Size the result exactly, so it needs no trimming copy: decrypt the
         # trailer block first (GPU), apply unpad_final's rule to it, then
         # decrypt the leading n-16 bytes as a non-final chunk straight into
-        # the result and append the trailer's unpadded part.
+        # the result and append the trailer's unpadded part.  (Up to
+        # _TRIM_COPY_MAX bytes one call and a trimming copy are cheaper than
+        # the extra call: decrypt_bytes of 16 KiB 42 -> ~27 us.)
         last = C.create_string_buffer(BLOCK)
         _raise(L.paes_cuda_ecb(DECRYPT, src.ptr + src.n - BLOCK, last, BLOCK, rk, 1))
         keep = L.paes_cuda_unpad_final(last, BLOCK)
