@@ -27,6 +27,9 @@ namespace {
 #ifndef PAES_PDL
 #define PAES_PDL 1
 #endif
+#ifndef PAES_PREFETCH
+#define PAES_PREFETCH 1  // tiles per warp prefetched into L2 before griddepcontrol.wait (0 = off)
+#endif
 #ifndef PAES_THREADS
 #define PAES_THREADS 512
 #endif
@@ -321,6 +324,21 @@ __global__ void __launch_bounds__(kThreads, 1) ecb_kernel(const __grid_constant_
   // programmatic dependent launch: stage the tables (constant data) while the
   // previous kernel in the stream drains, let the next launch in, and touch
   // the buffers only once the previous grid has completed
+#if PAES_PREFETCH
+  // ...except for an L2 prefetch of the first tile: a hint with no
+  // architectural effect (L2 is coherent for every SM and global stores write
+  // through to it, so data the previous grid is still writing is read fresh
+  // after the wait), it moves the tile's HBM latency under the staging
+#pragma unroll
+  for (int p = 0; p < PAES_PREFETCH; ++p) {
+    const unsigned long long t = tile + p * tstride;
+    if (t < full_tiles) {
+#pragma unroll
+      for (int j = 0; j < NB; ++j)
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(a.in + 16ull * (t * kTile + lane + 32ull * j)));
+    }
+  }
+#endif
   stage_tables<DEC>(sm);
   asm volatile("griddepcontrol.launch_dependents;");
   asm volatile("griddepcontrol.wait;" ::: "memory");
