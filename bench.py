@@ -646,11 +646,14 @@ class ConfigBench:
         return self.torch.empty(max(n, 16) + 64, dtype=self.torch.uint8, pin_memory=True)
 
     def queued(self, fns):
-        """One event pair around len(fns) queued calls; returns ms per call."""
+        """One event pair around len(fns) queued calls; returns ms per call.
+        The start event is queued behind the warm-up calls (no sync between),
+        so the timed calls start back to back on a busy stream and the host's
+        issue latency for the first of them is not counted as device time."""
         torch = self.torch
+        self.s.synchronize()
         for f in fns[: self.warmup]:
             f()
-        self.s.synchronize()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record(self.s)
         for f in fns:
