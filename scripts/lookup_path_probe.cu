@@ -24,7 +24,10 @@
 constexpr int kThreads = 512;
 constexpr int kChains = 8;
 
-enum Path { LDS = 0, LDG = 1, TEX = 2, ALU = 3 };
+enum Path { LDS = 0, LDG = 1, TEX = 2, ALU = 3, LDC = 4, MIX = 5 };
+
+__constant__ unsigned c_tab[256];
+constexpr int kMixLdc = 3;  // MIX: per chain round, 32 LDS lookups + this many LDC lookups (~ the last round's share)
 
 template <int P>
 __device__ __forceinline__ unsigned look(unsigned x, int k, const char* smb, unsigned lane4, const unsigned* g,
@@ -35,6 +38,8 @@ __device__ __forceinline__ unsigned look(unsigned x, int k, const char* smb, uns
     return __ldg(g + ((x >> (8 * k)) & 255));
   } else if constexpr (P == TEX) {
     return tex1Dfetch<unsigned>(t, (x >> (8 * k)) & 255);
+  } else if constexpr (P == LDC) {
+    return c_tab[(x >> (8 * k)) & 255];  // indexed constant load, divergent addresses
   } else {
     // ALU stand-in of similar instruction weight: two rotations and an add
     return __funnelshift_l(x, x, 5 + k) + (x >> 3);
@@ -48,8 +53,15 @@ __device__ __forceinline__ void run(unsigned (&c)[kChains], int iters, const cha
 #pragma unroll
     for (int j = 0; j < kChains; ++j) {
       const unsigned x = c[j];
-      c[j] = look<P>(x, 0, smb, lane4, g, t) ^ look<P>(x, 1, smb, lane4, g, t) ^
-             look<P>(x, 2, smb, lane4, g, t) ^ look<P>(x, 3, smb, lane4, g, t) ^ (x * 0x9e3779b9u);
+      if constexpr (P == MIX) {
+        unsigned v = look<LDS>(x, 0, smb, lane4, g, t) ^ look<LDS>(x, 1, smb, lane4, g, t) ^
+                     look<LDS>(x, 2, smb, lane4, g, t) ^ look<LDS>(x, 3, smb, lane4, g, t) ^ (x * 0x9e3779b9u);
+        if (j < kMixLdc) v ^= look<LDC>(x, j, smb, lane4, g, t);
+        c[j] = v;
+      } else {
+        c[j] = look<P>(x, 0, smb, lane4, g, t) ^ look<P>(x, 1, smb, lane4, g, t) ^
+               look<P>(x, 2, smb, lane4, g, t) ^ look<P>(x, 3, smb, lane4, g, t) ^ (x * 0x9e3779b9u);
+      }
     }
   }
 }
@@ -75,6 +87,8 @@ probe(int pa, int pb, int iters, const unsigned* g, cudaTextureObject_t t, unsig
     case LDG: run<LDG>(c, iters, smb, lane4, g, t); break;
     case TEX: run<TEX>(c, iters, smb, lane4, g, t); break;
     case ALU: run<ALU>(c, iters, smb, lane4, g, t); break;
+    case LDC: run<LDC>(c, iters, smb, lane4, g, t); break;
+    case MIX: run<MIX>(c, iters, smb, lane4, g, t); break;
     default: break;
   }
   unsigned acc = 0;
@@ -97,6 +111,7 @@ int main() {
   long long* clk;
   CK(cudaMalloc(&g, sizeof h));
   CK(cudaMemcpy(g, h, sizeof h, cudaMemcpyHostToDevice));
+  CK(cudaMemcpyToSymbol(c_tab, h, sizeof h));
   CK(cudaMalloc(&sink, 4));
   CK(cudaMalloc(&clk, 16));
   cudaResourceDesc rd{};
@@ -115,7 +130,8 @@ int main() {
     int pa, pb;
   } cases[] = {{"lds_all", LDS, LDS},  {"lds_half", LDS, -1},  {"ldg_all", LDG, LDG},
                {"tex_all", TEX, TEX},  {"lds+ldg", LDS, LDG},  {"lds+tex", LDS, TEX},
-               {"lds+alu", LDS, ALU},  {"alu_all", ALU, ALU}};
+               {"lds+alu", LDS, ALU},  {"alu_all", ALU, ALU},  {"ldc_all", LDC, LDC},  {"ldc_half", LDC, -1},
+               {"lds+ldc", LDS, LDC},  {"mix_32lds_3ldc_all", MIX, MIX}};
   const int iters = 2000;
   cudaEvent_t e0, e1;
   CK(cudaEventCreate(&e0));
@@ -141,7 +157,8 @@ int main() {
       }
     }
     // lookups: 4 per chain step for each warp on a lookup path
-    auto lk = [&](int p) { return (p == LDS || p == LDG || p == TEX) ? 1.0 : 0.0; };
+    // (MIX counts its LDS lookups only: compare its ms with lds_all's)
+    auto lk = [&](int p) { return (p == LDS || p == LDG || p == TEX || p == LDC || p == MIX) ? 1.0 : 0.0; };
     const double warps = kThreads / 32.0;
     const double lookups = (lk(cs.pa) + lk(cs.pb)) * (warps / 2) * 32 * (double)iters * kChains * 4 * sms;
     const double per_clk_sm = lookups / sms / (double)cyc;
