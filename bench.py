@@ -325,12 +325,17 @@ def cpu_baseline(args):
             t = time.perf_counter()
             R.threads_into(0, pt.ctypes.data, pt.nbytes, key, ct.ctypes.data, workers)
             samples.append(time.perf_counter() - t)
+        # W = 1 beside W = all cores: the reference's per-core rate
+        one = min(pt.nbytes, 64 * MiB)
+        t = time.perf_counter()
+        R.threads_into(0, pt.ctypes.data, one, key, ct.ctypes.data, 1)
+        single = one / (time.perf_counter() - t) / 1e9
     finally:
         os.sched_setaffinity(0, bound)
     kept = R.reject_outliers(samples)  # the reference's own method (bench.cpp:49-79)
     avg = sum(kept) / len(kept)
     return {"value": round(pt.nbytes / avg / 1e9, 4), "unit": "GB/s", "cores": workers, "physical_cores": phys,
-            "kind": "reference",
+            "kind": "reference", "single_thread_value": round(single, 4),
             "sample": f"{pt.nbytes} B of the config-4 stream, 5 reps, reject_outliers mean "
                       f"(reference paes_core compiled from its sources, {workers} threads)",
             "seconds": [round(x, 4) for x in samples]}
