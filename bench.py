@@ -1002,6 +1002,13 @@ class ConfigBench:
                 return sec
 
             gpu = cell(lambda: paes.encrypt_file(src, ct, key, workers=ngpu, strategy="gpu")["seconds"], ngpu, "gpu")
+            # the same jobs by the caller's wall clock, back to back: includes what
+            # JobOutcome.seconds leaves out (unmapping the output, the detached
+            # reclaim of the replaced file competing with the next job)
+            t_loop = time.perf_counter()
+            for _ in range(3):
+                paes.encrypt_file(src, ct, key, workers=ngpu, strategy="gpu")
+            loop_wall = (time.perf_counter() - t_loop) / 3
             ok = hashlib.sha256(open(ct, "rb").read()).hexdigest() == e["ct_sha256"]
             dec = cell(lambda: paes.decrypt_file(ct, pt, key, workers=ngpu, strategy="gpu")["seconds"], ngpu, "gpu")
             ok = ok and hashlib.sha256(open(pt, "rb").read()).hexdigest() == e["pt_sha256"]
@@ -1016,6 +1023,10 @@ class ConfigBench:
                                 f"measure_cell: 1 warm + 3 reps, reject_outliers mean)",
                     "value": round(n / gpu.avg_seconds / 1e9, 3), "unit": "GB/s", "mbps": round(gpu.throughput_mbps, 1),
                     "decrypt_value": round(m / dec.avg_seconds / 1e9, 3),
+                    "loop_wall_value": round(n / loop_wall / 1e9, 3),
+                    "note": "each rep replaces the previous output; the engine frees the replaced file's pages on a "
+                            "detached thread (abi_file.cu ReplacedOutput), the reference inside its rename; "
+                            "loop_wall_value = 3 back-to-back calls by the caller's wall clock",
                     "api": "paes_cuda_run_job (strategy gpu: pread -> pinned ring -> GPU -> writer, temp + rename)",
                     "seconds": [round(x, 4) for x in gpu.samples],
                     "process_strategy_gpu_worker": {

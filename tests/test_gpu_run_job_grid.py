@@ -109,6 +109,46 @@ def test_large_file_parallel_io_and_pwrite_path(paes, gpu, ref, eight_workers, t
         assert (tmp_path / "back.bin").read_bytes() == data, workers
 
 
+@pytest.mark.parametrize("reclaim", ["1", "0"])
+def test_replacing_a_large_output(paes, gpu, ref, tmp_path, monkeypatch, reclaim):
+    """AtomicOutput (exec.cpp:80-106) when the output already exists and is
+    large: the engine renames over it and frees the old file's pages on a
+    detached thread (abi_file.cu ReplacedOutput; PAES_FILE_ASYNC_RECLAIM=0 =
+    inside rename).  A reader that had the old output open keeps the old
+    bytes, a hard link to it keeps them too, repeated jobs give the same
+    ciphertext, and a failing job leaves the existing output untouched."""
+    monkeypatch.setenv("PAES_FILE_ASYNC_RECLAIM", reclaim)
+    rnd = random.Random(77)
+    key = rnd.randbytes(16)
+    data = rnd.randbytes((72 << 20) + 5)  # above the 64 MiB threshold of the deferred reclaim
+    src, out, link = tmp_path / "plain.bin", tmp_path / "c.enc", tmp_path / "c.link"
+    src.write_bytes(data)
+    rc, _, _, _ = ref.run_job(str(src), str(tmp_path / "ref.enc"), key, 1, 0, 0)
+    assert rc == 0
+    expected = (tmp_path / "ref.enc").read_bytes()
+    old = bytes(80 << 20)
+    out.write_bytes(old)
+    with open(out, "rb") as held:
+        paes.encrypt_file(str(src), str(out), key, strategy="gpu", workers=1)
+        assert out.read_bytes() == expected
+        assert held.read() == old  # the replaced inode lives while someone holds it
+    for _ in range(3):  # each job replaces the previous (large) output
+        paes.encrypt_file(str(src), str(out), key, strategy="gpu", workers=1)
+        assert out.read_bytes() == expected
+    os.link(out, link)  # two names: not ours to reclaim; both stay valid
+    paes.encrypt_file(str(src), str(out), key, strategy="gpu", workers=1)
+    assert out.read_bytes() == expected and link.read_bytes() == expected
+    # a failing decrypt (wrong key) must leave the existing large output alone
+    back = tmp_path / "p.bin"
+    back.write_bytes(old)
+    bad = bytes([key[0] ^ 1]) + key[1:]
+    with pytest.raises((paes.WorkerError, paes.PaddingError)):
+        paes.decrypt_file(str(out), str(back), bad, strategy="gpu", workers=1)
+    assert back.read_bytes() == old
+    paes.decrypt_file(str(out), str(back), key, strategy="gpu", workers=1)
+    assert back.read_bytes() == data
+
+
 def test_unknown_device_is_enodev(paes, gpu):
     from paper_1403_7295_b200 import _native as N
 
