@@ -2,6 +2,9 @@
 // (run_job's output side, abi_file.cu.)  Page faults of a fresh shared mapping
 // contend on the file's page-cache lock; this probe times the alternatives:
 //   mmap_copy        T threads memcpy into a fresh MAP_SHARED mapping (the current writer)
+//   mmap_copyK       the same with K < T threads
+//   populateSM_copy  T threads madvise(MADV_POPULATE_WRITE) S MiB of the mapping at a time, then memcpy it
+//   mmap_copy_after_falloc  one fallocate, then T threads memcpy through the mapping
 //   pwrite           T threads pwrite into the fresh file (pages allocated by write, not zeroed first)
 //   falloc1+pwrite   one thread fallocates everything, then T threads pwrite
 //   fallocK          K threads fallocate disjoint ranges (time only)
@@ -66,6 +69,49 @@ int main(int argc, char** argv) {
       ::munmap(p, n);
       ::close(fd);
       std::printf(", \"mmap_copy_s_%d\": %.3f", rep, c - a);
+    }
+    for (unsigned tt : {t / 2, t / 4, t / 8}) {  // fewer faulting threads: is the fault path contended?
+      if (!tt) continue;
+      const int fd = fresh();
+      const double a = now();
+      (void)!::ftruncate(fd, static_cast<off_t>(n));
+      auto* p = static_cast<char*>(::mmap(nullptr, n, PROT_READ | PROT_WRITE, MAP_SHARED, fd, 0));
+      par(tt, n, [&](std::size_t b, std::size_t l) { std::memcpy(p + b, src.data() + b, l); });
+      const double c = now();
+      ::munmap(p, n);
+      ::close(fd);
+      std::printf(", \"mmap_copy%u_s_%d\": %.3f", tt, rep, c - a);
+    }
+    for (std::size_t step : {std::size_t(2) << 20, std::size_t(32) << 20}) {
+      // each thread populates (allocate + zero + map, no per-page trap) a step of its range, then copies it
+      const int fd = fresh();
+      const double a = now();
+      (void)!::ftruncate(fd, static_cast<off_t>(n));
+      auto* p = static_cast<char*>(::mmap(nullptr, n, PROT_READ | PROT_WRITE, MAP_SHARED, fd, 0));
+      par(t, n, [&](std::size_t b, std::size_t l) {
+        for (std::size_t o = 0; o < l; o += step) {
+          const std::size_t m = std::min(step, l - o);
+          if (::madvise(p + b + o, m, 23 /* MADV_POPULATE_WRITE */) != 0) { std::perror("madvise"); }
+          std::memcpy(p + b + o, src.data() + b + o, m);
+        }
+      });
+      const double c = now();
+      ::munmap(p, n);
+      ::close(fd);
+      std::printf(", \"populate%zuM_copy_s_%d\": %.3f", step >> 20, rep, c - a);
+    }
+    {
+      // one fallocate (allocation only), then T threads copy through the mapping (faults zero + map)
+      const int fd = fresh();
+      const double a = now();
+      (void)!::posix_fallocate(fd, 0, static_cast<off_t>(n));
+      const double b0 = now();
+      auto* p = static_cast<char*>(::mmap(nullptr, n, PROT_READ | PROT_WRITE, MAP_SHARED, fd, 0));
+      par(t, n, [&](std::size_t b, std::size_t l) { std::memcpy(p + b, src.data() + b, l); });
+      const double c = now();
+      ::munmap(p, n);
+      ::close(fd);
+      std::printf(", \"mmap_copy_after_falloc_s_%d\": %.3f", rep, c - b0);
     }
     for (unsigned tt : {t, t / 2, t / 4}) {
       const int fd = fresh();
