@@ -10,14 +10,18 @@
 
 #include <cerrno>
 #include <chrono>
+#include <cstdio>
 #include <sstream>
 #include <thread>
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
+#include <condition_variable>
 #include <cstdlib>
 #include <cstring>
 #include <memory>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -47,6 +51,125 @@ struct Map {
   ~Map() {
     if (p) ::munmap(p, n);
   }
+};
+
+// The pages of a mapped output, allocated ahead of the writers.  A store to a
+// fresh page of a shared tmpfs mapping allocates, zeroes and maps it inside the
+// fault, and 8-16 threads faulting one file saturate at ~0.55 s per 4 GiB
+// (scripts/file_write_probe.cpp: 1 thread 2.2 s, 4 threads 0.69, 8 0.53, 16
+// 0.56).  fallocate(2) allocates the same pages without zeroing or mapping
+// them at 0.30 s per 4 GiB from one thread (more threads serialise on the
+// inode), and copies into already allocated pages then take 0.14-0.16 s with
+// 16 threads.  So one thread runs fallocate over the shards' output regions in
+// steps, round-robin, and each writer waits until the step holding its bytes is
+// allocated: allocation overlaps the reads, the GPU and the copies instead of
+// sitting inside every fault.  (Round 1 measured one fallocate of the whole
+// file on a side thread with writers NOT waiting for it: slower, the faults
+// and the allocator fought over the same pages.)  It also reserves the space:
+// when the file system fills up, fallocate fails and the writers raise IoError
+// instead of taking SIGBUS on a page that cannot be backed.
+// PAES_FILE_PREALLOC=0 turns it off (writers fault the pages in themselves).
+// Measured in the job (scripts/file_reclaim_ab.py --env PAES_FILE_PREALLOC,
+// profiles/r02_file_prealloc_ab.json, 4 GiB on /dev/shm): 0.60-0.62 -> 0.52-0.55
+// s.  The allocator is then the critical path and runs at ~0.5 s per 4 GiB, not
+// its 0.30 s alone: the writers' faults on the same inode slow it.  Letting
+// allocator and writers take turns on a shared_mutex, which in isolation gets
+// the sum 0.30 + 0.16 s (file_write_probe turns_*), gave no gain in the job
+// (0.60-0.61 s) and was dropped.
+class Prealloc {
+ public:
+  struct Region {
+    std::uint64_t off = 0, len = 0;
+  };
+  static constexpr std::uint64_t kStep = 16ull << 20;
+
+  Prealloc() = default;
+  Prealloc(const Prealloc&) = delete;
+  Prealloc& operator=(const Prealloc&) = delete;
+  ~Prealloc() { stop(); }
+
+  void start(int fd, std::vector<Region> regions) {
+    const char* e = std::getenv("PAES_FILE_PREALLOC");
+    if ((e && e[0] == '0') || regions.empty()) return;
+    fd_ = fd;
+    regions_ = std::move(regions);
+    done_.assign(regions_.size(), 0);
+    active_ = true;
+    th_ = std::thread([this] { run(); });
+  }
+  bool active() const { return active_; }
+
+  // Blocks until bytes [off, off + len) of the file are allocated; false when
+  // the allocation failed (the caller reports the write failure).
+  bool wait(std::uint64_t off, std::uint64_t len) {
+    if (!active_ || !len) return true;
+    std::size_t r = 0;
+    while (r < regions_.size() && !(off >= regions_[r].off && off < regions_[r].off + regions_[r].len)) ++r;
+    if (r == regions_.size()) return true;  // outside every region: nothing was promised
+    const std::uint64_t need = std::min(off + len - regions_[r].off, regions_[r].len);
+    const auto t0 = std::chrono::steady_clock::now();
+    std::unique_lock<std::mutex> lk(mu_);
+    cv_.wait(lk, [&] { return done_[r] >= need || failed_ || unsupported_; });
+    waited_ns_ += std::chrono::duration_cast<std::chrono::nanoseconds>(std::chrono::steady_clock::now() - t0).count();
+    return !failed_;
+  }
+
+  void stop() {
+    if (!th_.joinable()) return;
+    quit_.store(true, std::memory_order_relaxed);
+    th_.join();
+  }
+
+ private:
+  void run() {
+    const auto t0 = std::chrono::steady_clock::now();
+    struct Trace {
+      std::chrono::steady_clock::time_point t0;
+      Prealloc* self;
+      ~Trace() {
+        if (std::getenv("PAES_FILE_TRACE"))
+          std::fprintf(stderr, "[paes file] prealloc thread ran %.3f s; writers waited %.3f s in total\n",
+                       std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count(),
+                       self->waited_ns_.load() * 1e-9);
+      }
+    } trace{t0, this};
+    std::vector<std::uint64_t> pos(regions_.size(), 0);
+    for (bool more = true; more && !quit_.load(std::memory_order_relaxed);) {
+      more = false;
+      for (std::size_t r = 0; r < regions_.size() && !quit_.load(std::memory_order_relaxed); ++r) {
+        if (pos[r] >= regions_[r].len) continue;
+        const std::uint64_t n = std::min(kStep, regions_[r].len - pos[r]);
+        int rc;
+        do {
+          rc = ::fallocate(fd_, 0, static_cast<off_t>(regions_[r].off + pos[r]), static_cast<off_t>(n));
+        } while (rc != 0 && errno == EINTR);
+        std::lock_guard<std::mutex> lk(mu_);
+        if (rc != 0) {
+          // no fallocate here: the writers allocate by faulting, as before;
+          // anything else (ENOSPC, EDQUOT, EIO, EFBIG) fails the job
+          if (errno == EOPNOTSUPP || errno == ENOSYS) unsupported_ = true;
+          else failed_ = true;
+          cv_.notify_all();
+          return;
+        }
+        pos[r] += n;
+        done_[r] = pos[r];
+        cv_.notify_all();
+        more = more || pos[r] < regions_[r].len;
+      }
+    }
+  }
+
+  int fd_ = -1;
+  std::vector<Region> regions_;
+  std::vector<std::uint64_t> done_;  // bytes allocated from each region's start (mu_)
+  std::mutex mu_;
+  std::condition_variable cv_;
+  bool failed_ = false, unsupported_ = false;  // mu_
+  bool active_ = false;
+  std::atomic<bool> quit_{false};
+  std::atomic<long long> waited_ns_{0};  // PAES_FILE_TRACE
+  std::thread th_;
 };
 
 // Size the output to `cap` and pick the writer by file system.  On tmpfs
@@ -79,9 +202,15 @@ void open_output(int fd, std::uint64_t cap, Map& map) {
   // the whole output; otherwise pwrite, whose ENOSPC becomes IoError and the
   // temp file is removed (AtomicOutput, exec.cpp:80-106).  (Reserving with
   // fallocate instead was measured slower on tmpfs, see above.)
+  // (PAES_FILE_SKIP_SPACE_CHECK=1 is a test hook: it lets the mapping through
+  // on a file system that is too small, as if the space had been taken between
+  // this check and the writes; the Prealloc thread's fallocate then fails and
+  // the job reports IoError.)
+  const char* skip = std::getenv("PAES_FILE_SKIP_SPACE_CHECK");
   struct statfs fs {};
-  if (::fstatfs(fd, &fs) != 0 ||
-      static_cast<unsigned long long>(fs.f_bavail) * static_cast<unsigned long long>(fs.f_bsize) < cap)
+  if (!(skip && skip[0] == '1') &&
+      (::fstatfs(fd, &fs) != 0 ||
+       static_cast<unsigned long long>(fs.f_bavail) * static_cast<unsigned long long>(fs.f_bsize) < cap))
     return;
   void* p = ::mmap(nullptr, cap, PROT_READ | PROT_WRITE, MAP_SHARED, fd, 0);
   if (p != MAP_FAILED) {
@@ -193,7 +322,7 @@ void par_io(std::uint64_t n, unsigned threads, F&& f) {
 // bytes [in_off, in_off + r.in_len) land at out_off in the output (run_job:
 // equal offsets; a worker chunk: its own file from 0).  Returns the output
 // bytes written (decrypt final: unpadded).
-std::uint64_t file_shard(DevCtx& d, const Range& r, int in_fd, int out_fd, std::uint8_t* out_map,
+std::uint64_t file_shard(DevCtx& d, const Range& r, int in_fd, int out_fd, std::uint8_t* out_map, Prealloc* pre,
                          std::uint64_t in_off, std::uint64_t out_off, const KeyWords& kw, const std::string& in_path,
                          const std::string& out_path, unsigned io_threads) {
   DeviceGuard g(d.id);
@@ -218,9 +347,11 @@ std::uint64_t file_shard(DevCtx& d, const Range& r, int in_fd, int out_fd, std::
       // both writers split the slot over the I/O threads: page faults of a
       // shared mapping proceed in parallel, and one pwrite per slot measured
       // slower on ext4 (1.22 vs 1.65 GB/s, 4 GiB)
-      if (out_map)
+      if (out_map) {
+        // the piece's pages are allocated ahead by the job's Prealloc thread
+        if (pre && !pre->wait(base, len)) throw IoFail{"write failed: " + out_path};
         par_io(len, io_threads, [&](std::uint64_t o, std::uint64_t n) { bulk_copy(out_map + base + o, slot + o, n); });
-      else
+      } else
         par_io(len, io_threads, [&](std::uint64_t o, std::uint64_t n) { pwrite_all(out_fd, slot + o, n, base + o, out_path); });
     } catch (const IoFail& e) {
       werr[s] = e.msg;
@@ -301,6 +432,13 @@ extern "C" int paes_cuda_run_job(const char* input_path, const char* output_path
     const std::uint64_t cap = dec ? len : (len / 16 + 1) * 16;
     Map map;
     open_output(out.fd, cap, map);
+    Prealloc pre;  // destroyed (joined) before the mapping and the descriptor go
+    if (map.p) {
+      std::vector<Prealloc::Region> regions;
+      for (const Chunk& c : plan)
+        regions.push_back({c.offset, dec ? c.raw_len : c.padded_len});
+      pre.start(out.fd, std::move(regions));
+    }
     std::vector<std::uint64_t> produced(plan.size(), 0);
     std::vector<std::string> failures(plan.size()), io_failures(plan.size());
     auto work = [&](std::size_t i) {
@@ -317,7 +455,7 @@ extern "C" int paes_cuda_run_job(const char* input_path, const char* output_path
         const unsigned io = g_io_threads_per_shard
                                 ? g_io_threads_per_shard
                                 : std::clamp<unsigned>(hw / static_cast<unsigned>(plan.size()), 1u, 8u);
-        produced[i] = file_shard(d, r, in.fd, out.fd, map.p, c.offset, c.offset, kw, in_path, tmp, io);
+        produced[i] = file_shard(d, r, in.fd, out.fd, map.p, &pre, c.offset, c.offset, kw, in_path, tmp, io);
       } catch (const CudaFail& e) {
         failures[i] = e.msg;
       } catch (const IoFail& e) {
@@ -343,6 +481,7 @@ extern "C" int paes_cuda_run_job(const char* input_path, const char* output_path
       any = true;
     }
     if (any) return fail(PAES_EWORKER, "worker failure: " + failed.str());
+    pre.stop();  // every region is allocated by now (each shard waited for its last piece)
     std::uint64_t total = 0;
     for (auto p : produced) total += p;
     if (::ftruncate(out.fd, static_cast<off_t>(total)) != 0) return fail(PAES_EIO, "truncate failed: " + tmp);
@@ -404,13 +543,16 @@ extern "C" int paes_cuda_worker_chunk(const char* input_path, uint64_t offset, u
       const std::uint64_t cap = r.pad ? (raw_len / 16 + 1) * 16 : raw_len;
       Map map;
       open_output(out.fd, cap, map);
+      Prealloc pre;
+      if (map.p) pre.start(out.fd, {{0, cap}});
       std::uint64_t produced = 0;
       if (cap) {
         DevCtx& d = rt::device(dev);
         std::lock_guard<std::mutex> lk(d.mu);
         const unsigned io = g_io_threads_per_shard ? g_io_threads_per_shard
                                                    : std::clamp<unsigned>(std::thread::hardware_concurrency(), 1u, 8u);
-        produced = file_shard(d, r, in.fd, out.fd, map.p, offset, 0, kw, in_path, out_path, io);
+        produced = file_shard(d, r, in.fd, out.fd, map.p, &pre, offset, 0, kw, in_path, out_path, io);
+        pre.stop();
       }
       if (::ftruncate(out.fd, static_cast<off_t>(produced)) != 0) throw IoFail{"truncate failed: " + out_path};
       return PAES_OK;

@@ -41,6 +41,9 @@ def main():
     ap.add_argument("--size", type=int, default=(4 << 30) + 7)
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--dir", default="/dev/shm")
+    ap.add_argument("--modes", default="0,1", help="values of the switch to compare")
+    ap.add_argument("--env", default="PAES_FILE_ASYNC_RECLAIM",
+                    help="the 0/1 switch to A/B (also PAES_FILE_PREALLOC: fallocate thread ahead of the mapped writers)")
     args = ap.parse_args()
     O = oracle.Oracle()
     key = O.sweep(3, 16)
@@ -51,13 +54,14 @@ def main():
     O.counter_fill_into(3, 0, args.size, buf.ctypes.data)
     buf.tofile(src)
     del buf
-    res = {"size": args.size, "dir": args.dir, "reps": args.reps}
+    res = {"size": args.size, "dir": args.dir, "reps": args.reps, "switch": args.env}
     try:
         paes.encrypt_file(src, ct, key, workers=1)  # warm: context, ring, page cache
         want_ct, want_pt = sha(ct), sha(src)
-        for order in (("0", "1"), ("1", "0")):  # both orders: no drift credit
+        modes = tuple(args.modes.split(","))
+        for order in (modes, modes[::-1]):  # both orders: no drift credit
             for mode in order:
-                os.environ["PAES_FILE_ASYNC_RECLAIM"] = mode
+                os.environ[args.env] = mode
                 for name, fn, out, want in (("enc", lambda: paes.encrypt_file(src, ct, key, workers=1), ct, want_ct),
                                             ("dec", lambda: paes.decrypt_file(ct, pt, key, workers=1), pt, want_pt)):
                     fn()
@@ -67,7 +71,7 @@ def main():
                     time.sleep(0.5)  # let a reaper finish before the digest read
                     ok = sha(out) == want
                     n = args.size
-                    res.setdefault(f"reclaim={mode}", []).append(
+                    res.setdefault(f"{args.env}={mode}", []).append(
                         {"op": name, "job_seconds": [round(x, 4) for x in secs],
                          "gbs_job_median": round(n / sorted(secs)[len(secs) // 2] / 1e9, 3),
                          "gbs_loop_wall": round(n * args.reps / wall / 1e9, 3), "parity": "ok" if ok else "MISMATCH"})

@@ -5,6 +5,8 @@
 //   mmap_copyK       the same with K < T threads
 //   populateSM_copy  T threads madvise(MADV_POPULATE_WRITE) S MiB of the mapping at a time, then memcpy it
 //   mmap_copy_after_falloc  one fallocate, then T threads memcpy through the mapping
+//   pipe_falloc_mmapW  one allocator thread in 16 MiB steps, W writers copy 64 MiB pieces through the mapping behind it
+//   turns_fallocSM_mmap  the same with S MiB steps, allocator and writers taking turns (never concurrent)
 //   pwrite           T threads pwrite into the fresh file (pages allocated by write, not zeroed first)
 //   falloc1+pwrite   one thread fallocates everything, then T threads pwrite
 //   fallocK          K threads fallocate disjoint ranges (time only)
@@ -21,6 +23,8 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
+#include <shared_mutex>
 #include <string>
 #include <thread>
 #include <vector>
@@ -112,6 +116,87 @@ int main(int argc, char** argv) {
       ::munmap(p, n);
       ::close(fd);
       std::printf(", \"mmap_copy_after_falloc_s_%d\": %.3f", rep, c - b0);
+    }
+    for (unsigned w : {t, t / 2, t / 4}) {
+      // one allocator thread runs ahead in 16 MiB steps; W writers copy each 64 MiB piece through the mapping
+      // once it is allocated (run_job's Prealloc, without the reads and the GPU)
+      if (!w) continue;
+      const int fd = fresh();
+      constexpr std::size_t kStep = 16u << 20, kPiece = 64u << 20;
+      std::atomic<std::size_t> mark{0};
+      const double a = now();
+      (void)!::ftruncate(fd, static_cast<off_t>(n));
+      auto* p = static_cast<char*>(::mmap(nullptr, n, PROT_READ | PROT_WRITE, MAP_SHARED, fd, 0));
+      double alloc_done = 0;
+      std::thread alloc([&] {
+        for (std::size_t o = 0; o < n; o += kStep) {
+          (void)!::fallocate(fd, 0, static_cast<off_t>(o), static_cast<off_t>(std::min(kStep, n - o)));
+          mark.store(std::min(n, o + kStep), std::memory_order_release);
+        }
+        alloc_done = now();
+      });
+      std::vector<std::thread> wr;
+      for (unsigned i = 0; i < w; ++i)
+        wr.emplace_back([&, i] {
+          for (std::size_t b = 0; b < n; b += kPiece) {
+            const std::size_t l = std::min(kPiece, n - b);
+            while (mark.load(std::memory_order_acquire) < b + l) std::this_thread::yield();
+            const std::size_t part = ((l + w - 1) / w + 4095) & ~std::size_t(4095);
+            const std::size_t pb = std::min(l, i * part), pe = std::min(l, (i + 1) * part);
+            if (pb < pe) std::memcpy(p + b + pb, src.data() + b + pb, pe - pb);
+          }
+        });
+      alloc.join();
+      for (auto& th : wr) th.join();
+      const double c = now();
+      ::munmap(p, n);
+      ::close(fd);
+      std::printf(", \"pipe_falloc_mmap%u_s_%d\": %.3f, \"pipe_falloc_mmap%u_alloc_done_s_%d\": %.3f", w, rep, c - a, w, rep,
+                  alloc_done - a);
+    }
+    for (std::size_t kStep : {std::size_t(16) << 20, std::size_t(64) << 20, std::size_t(256) << 20}) {
+      // the same, but allocator and writers never run at the same time: the allocator takes a lock exclusively per
+      // step, the writers share it while they copy (faults and fallocate on one inode slow each other down)
+      const unsigned w = t;
+      const int fd = fresh();
+      constexpr std::size_t kPiece = 64u << 20;
+      std::atomic<std::size_t> mark{0};
+      std::shared_mutex turn;
+      const double a = now();
+      (void)!::ftruncate(fd, static_cast<off_t>(n));
+      auto* p = static_cast<char*>(::mmap(nullptr, n, PROT_READ | PROT_WRITE, MAP_SHARED, fd, 0));
+      double alloc_done = 0;
+      std::thread alloc([&] {
+        for (std::size_t o = 0; o < n; o += kStep) {
+          {
+            std::unique_lock<std::shared_mutex> lk(turn);
+            (void)!::fallocate(fd, 0, static_cast<off_t>(o), static_cast<off_t>(std::min(kStep, n - o)));
+          }
+          mark.store(std::min(n, o + kStep), std::memory_order_release);
+        }
+        alloc_done = now();
+      });
+      std::vector<std::thread> wr;
+      for (unsigned i = 0; i < w; ++i)
+        wr.emplace_back([&, i] {
+          for (std::size_t b = 0; b < n; b += kPiece) {
+            const std::size_t l = std::min(kPiece, n - b);
+            while (mark.load(std::memory_order_acquire) < b + l) std::this_thread::yield();
+            const std::size_t part = ((l + w - 1) / w + 4095) & ~std::size_t(4095);
+            const std::size_t pb = std::min(l, i * part), pe = std::min(l, (i + 1) * part);
+            if (pb < pe) {
+              std::shared_lock<std::shared_mutex> lk(turn);
+              std::memcpy(p + b + pb, src.data() + b + pb, pe - pb);
+            }
+          }
+        });
+      alloc.join();
+      for (auto& th : wr) th.join();
+      const double c = now();
+      ::munmap(p, n);
+      ::close(fd);
+      std::printf(", \"turns_falloc%zuM_mmap_s_%d\": %.3f, \"turns_falloc%zuM_alloc_done_s_%d\": %.3f", kStep >> 20, rep, c - a,
+                  kStep >> 20, rep, alloc_done - a);
     }
     for (unsigned tt : {t, t / 2, t / 4}) {
       const int fd = fresh();

@@ -179,11 +179,14 @@ def test_staged_ring_large_pageable_matches_device_path(paes, gpu):
         assert np.array_equal(inplace[:n], src), n
 
 
-@pytest.mark.parametrize("writer", [None, "mmap", "pwrite"])
+@pytest.mark.parametrize("writer", [None, "mmap", "pwrite", "mmap_space_taken_after_the_check"])
 def test_run_job_on_a_full_tmpfs_is_ioerror_without_partial_output(paes, gpu, tmp_path, writer, monkeypatch):
     """An output tmpfs too small for the result: IoError (OSError), no SIGBUS
     from the shared-mapping writer, and no <out>.part.<pid> left behind
-    (AtomicOutput, exec.cpp:80-106)."""
+    (AtomicOutput, exec.cpp:80-106).  The last case skips the free-space check
+    (as if the space went away after it): the output is mapped, the Prealloc
+    thread's fallocate fails with ENOSPC and the writers report it instead of
+    storing into pages that cannot be backed."""
     import subprocess
 
     mnt = tmp_path / "small_tmpfs"
@@ -191,7 +194,10 @@ def test_run_job_on_a_full_tmpfs_is_ioerror_without_partial_output(paes, gpu, tm
     if subprocess.run(["mount", "-t", "tmpfs", "-o", "size=1m", "tmpfs", str(mnt)], capture_output=True).returncode:
         pytest.skip("cannot mount a tmpfs here")
     try:
-        if writer:
+        if writer == "mmap_space_taken_after_the_check":
+            monkeypatch.setenv("PAES_FILE_WRITER", "mmap")
+            monkeypatch.setenv("PAES_FILE_SKIP_SPACE_CHECK", "1")
+        elif writer:
             monkeypatch.setenv("PAES_FILE_WRITER", writer)
         src = tmp_path / "in.bin"
         src.write_bytes(os.urandom(4 << 20))
@@ -200,6 +206,7 @@ def test_run_job_on_a_full_tmpfs_is_ioerror_without_partial_output(paes, gpu, tm
         assert isinstance(ei.value, paes.IoError), ei.value
         assert os.listdir(mnt) == []
         # the engine is still usable: a job that fits goes through
+        monkeypatch.delenv("PAES_FILE_SKIP_SPACE_CHECK", raising=False)
         small = tmp_path / "small.bin"
         small.write_bytes(os.urandom(100_000))
         assert paes.encrypt_file(str(small), str(mnt / "ok.bin"), bytes(16))["bytes_out"] == 100_000 // 16 * 16 + 16
