@@ -231,11 +231,15 @@ void open_output(int fd, std::uint64_t cap, Map& map) {
 struct ReplacedOutput {
   int fd = -1;
   explicit ReplacedOutput(const char* path) {
+    // 0 = off, unset or 1 = files of at least 64 MiB, any other number = that
+    // many bytes (the sanitizer stress lowers it to reach this path with small files)
     const char* e = std::getenv("PAES_FILE_ASYNC_RECLAIM");
-    if (e && e[0] == '0') return;
+    const unsigned long long v = e ? std::strtoull(e, nullptr, 10) : 1;
+    if (v == 0) return;
+    const long long min_size = v == 1 ? (64ll << 20) : static_cast<long long>(v);
     fd = ::open(path, O_RDONLY | O_CLOEXEC);
     struct stat st {};
-    if (fd >= 0 && (::fstat(fd, &st) != 0 || !S_ISREG(st.st_mode) || st.st_nlink != 1 || st.st_size < (64ll << 20))) {
+    if (fd >= 0 && (::fstat(fd, &st) != 0 || !S_ISREG(st.st_mode) || st.st_nlink != 1 || st.st_size < min_size)) {
       ::close(fd);
       fd = -1;
     }

@@ -29,6 +29,9 @@ PY
 else
   mkdir -p gpurun_out
   log="gpurun_out/${san}_stress.log"
+  # the file jobs' helper threads too: mapped writer + fallocate thread on any
+  # file system, detached reclaim of replaced outputs from 4 KiB up
+  export PAES_FILE_WRITER="${PAES_FILE_WRITER:-mmap}" PAES_FILE_ASYNC_RECLAIM="${PAES_FILE_ASYNC_RECLAIM:-4096}"
   if [ "$san" = tsan ]; then
     # The CUDA driver's launch path copies kernel parameters into driver-owned
     # buffers under its own synchronisation, which TSAN cannot see; races whose

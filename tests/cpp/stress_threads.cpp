@@ -115,6 +115,9 @@ static void worker(int id, int iters) {
         }
         paes_job_outcome o{};
         EXPECT(paes_cuda_run_job((base + ".in").c_str(), (base + ".enc").c_str(), key, 2, 0, &o) == 0, "file encrypt");
+        // again over the existing output: the replaced file goes to the detached reclaim when it is large
+        // enough (PAES_FILE_ASYNC_RECLAIM lowers the threshold in the sanitizer runs)
+        EXPECT(paes_cuda_run_job((base + ".in").c_str(), (base + ".enc").c_str(), key, 1, 0, &o) == 0, "file re-encrypt");
         EXPECT(paes_cuda_run_job((base + ".enc").c_str(), (base + ".out").c_str(), key, 3, 1, &o) == 0, "file decrypt");
         std::ifstream g(base + ".out", std::ios::binary);
         std::vector<std::uint8_t> got((std::istreambuf_iterator<char>(g)), std::istreambuf_iterator<char>());
