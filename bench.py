@@ -965,6 +965,34 @@ class ConfigBench:
                 "api": "paes.encrypt_bytes / decrypt_bytes (the _paes drop-in; library-staged pinned ring)",
                 "parity": "ok" if ok else "MISMATCH"}
 
+    # -- the C++ drop-in: paes::gpu::encrypt_chunk / decrypt_chunk (include/paes_gpu.hpp, the reference's
+    #    exec.hpp:61-65 signatures) on a 4 GiB + 7 std::vector, compiled here with the box's g++
+    def cpp_shim(self):
+        from paper_1403_7295_b200 import _native
+
+        cxx = "/usr/bin/g++" if os.path.exists("/usr/bin/g++") else shutil.which("g++")
+        if not cxx:
+            return {"skipped": "no g++ on this box"}
+        libdir = os.path.dirname(_native.lib_path())
+        n = self.big[1]["len"]
+        with tempfile.TemporaryDirectory() as d:
+            exe = os.path.join(d, "shim_chunk_probe")
+            r = subprocess.run([cxx, "-std=c++20", "-O2", f"-I{os.path.join(ROOT, 'include')}",
+                                os.path.join(ROOT, "scripts", "shim_chunk_probe.cpp"), "-o", exe, f"-L{libdir}",
+                                "-lpaes_cuda", f"-Wl,-rpath,{libdir}"], capture_output=True, text=True)
+            if r.returncode:
+                return {"skipped": "shim probe did not compile: " + r.stderr[-300:]}
+            r = subprocess.run([exe, str(n - 7)], capture_output=True, text=True, timeout=600)
+            if r.returncode:
+                return {"error": "shim probe failed: " + (r.stdout + r.stderr)[-300:]}
+        row = json.loads(r.stdout.strip().splitlines()[-1])[str(n)]
+        return {"workload": f"paes::gpu::encrypt_chunk / decrypt_chunk on a {n} B std::vector (pageable), result returned "
+                            "as std::vector; best of 3 after a warm call",
+                "value": row["encrypt_gbs"], "unit": "GB/s", "decrypt_value": row["decrypt_gbs"],
+                "h2d_bytes_per_step": n, "d2h_bytes_per_step": (n // 16 + 1) * 16,
+                "api": "include/paes_gpu.hpp over paes_cuda_chunk (scripts/shim_chunk_probe.cpp)",
+                "parity": "ok (round trip)" if row["round_trip"] == "ok" else "MISMATCH"}
+
     # -- the paper's own metric: file -> file run_job, next to the reference's,
     #    through the reference's own harness contract (measure_cell + CSV)
     def file_e2e(self):
@@ -1068,7 +1096,7 @@ def run_configs(args, torch, paes, dev, sms):
                 if isinstance(row, dict) and "pipe_frac" in row:
                     row["pipe_frac"] = round(row["pipe_frac"] * scale, 4)
     out["clocks"] = clocks
-    for name, fn in [("e2e_pageable", cb.pageable), ("file_e2e", cb.file_e2e)]:
+    for name, fn in [("e2e_pageable", cb.pageable), ("e2e_cpp_shim", cb.cpp_shim), ("file_e2e", cb.file_e2e)]:
         try:
             out[name] = fn() if cb.big is not None else {"skipped": "config 3's 4 GiB input unavailable"}
         except Exception as e:

@@ -180,11 +180,40 @@ inline Block decrypt_block(const Block& in, const RoundKeySchedule& ks) {
 }
 
 // ---- chunk transforms (exec.hpp:61-65) --------------------------------------
+namespace detail {
+// The result vector of a chunk transform.  `std::vector<uint8_t>(n)` zero-fills
+// its n bytes on the calling thread before the engine overwrites every one of
+// them: for a 4 GiB chunk that single-threaded fill (page faults included)
+// costs several times the whole GPU call.  With libstdc++ the storage of a
+// large result is therefore reserved and the size set without touching it, so
+// its pages are first touched by the engine's parallel host copies (the same
+// idea as folly::resizeWithoutInitialization; the reference's signature, a
+// plain std::vector, is kept).  Other standard libraries, libstdc++'s debug
+// and sanitizer-annotated vectors, small results and -DPAES_GPU_NO_UNINIT take
+// the ordinary zero-filled vector.
+inline std::vector<std::uint8_t> result_bytes(std::size_t n) {
+#if defined(__GLIBCXX__) && !defined(_GLIBCXX_DEBUG) && !defined(_GLIBCXX_SANITIZE_VECTOR) && !defined(PAES_GPU_NO_UNINIT)
+  if (n >= (std::size_t(1) << 20)) {
+    struct Raw : std::vector<std::uint8_t> {
+      void set_size_uninitialized(std::size_t m) {
+        this->reserve(m);
+        this->_M_impl._M_finish = this->_M_impl._M_start + m;
+      }
+    };
+    Raw r;
+    r.set_size_uninitialized(n);
+    return std::vector<std::uint8_t>(std::move(r));
+  }
+#endif
+  return std::vector<std::uint8_t>(n);
+}
+}  // namespace detail
+
 inline std::vector<std::uint8_t> encrypt_chunk(std::span<const std::uint8_t> raw, bool is_final,
                                                const RoundKeySchedule& ks, int ngpus = 0) {
   if (!is_final && raw.size() % kBlockSize != 0)
     throw std::invalid_argument("non-final chunk length must be a multiple of 16");
-  std::vector<std::uint8_t> out(is_final ? (raw.size() / kBlockSize + 1) * kBlockSize : raw.size());
+  std::vector<std::uint8_t> out = detail::result_bytes(is_final ? (raw.size() / kBlockSize + 1) * kBlockSize : raw.size());
   std::uint64_t n = 0;
   check(paes_cuda_chunk(PAES_ENCRYPT, raw.data(), raw.size(), is_final ? 1 : 0, ks.data(), out.data(), &n, ngpus));
   out.resize(n);
@@ -193,7 +222,7 @@ inline std::vector<std::uint8_t> encrypt_chunk(std::span<const std::uint8_t> raw
 
 inline std::vector<std::uint8_t> decrypt_chunk(std::span<const std::uint8_t> cipher, bool is_final,
                                                const RoundKeySchedule& ks, int ngpus = 0) {
-  std::vector<std::uint8_t> out(cipher.size());
+  std::vector<std::uint8_t> out = detail::result_bytes(cipher.size());
   std::uint64_t n = 0;
   check(paes_cuda_chunk(PAES_DECRYPT, cipher.data(), cipher.size(), is_final ? 1 : 0, ks.data(), out.data(), &n,
                         ngpus));

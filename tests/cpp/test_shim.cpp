@@ -165,12 +165,19 @@ static void gpu_tests() {
   CHECK(back == zeros);
   // chunk round trips across ragged sizes (test_exec.cpp:64-86, 139-155)
   std::mt19937_64 rng(101);
-  for (std::size_t n : {0ul, 1ul, 15ul, 16ul, 17ul, 31ul, 32ul, 1000ul, 65536ul, 1ul << 20}) {
+  // from 1 MiB up the result vectors are sized without being zero-filled first (detail::result_bytes)
+  for (std::size_t n : {0ul, 1ul, 15ul, 16ul, 17ul, 31ul, 32ul, 1000ul, 65536ul, (1ul << 20) - 16, 1ul << 20, (1ul << 20) + 5,
+                        (9ul << 20) + 3}) {
     std::vector<std::uint8_t> data(n);
     for (auto& x : data) x = static_cast<std::uint8_t>(rng());
     const auto c = gpu::encrypt_chunk(data, true, ks);
     CHECK(c.size() == (n / 16 + 1) * 16);
     CHECK(gpu::decrypt_chunk(c, true, ks) == data);
+    if (n >= (1ul << 20)) {  // a failing call on the untouched-vector path: PaddingError, nothing leaked or torn
+      gpu::Key128 other{};
+      other.bytes[5] = 0x5a;
+      CHECK(throws<gpu::PaddingError>([&] { gpu::decrypt_chunk(c, true, gpu::RoundKeySchedule(other)); }));
+    }
     // region independence (test_exec.cpp:291-312): two chunks == one final chunk
     if (n >= 32 && n % 16 == 0) {
       const auto first = gpu::encrypt_chunk(std::span(data).subspan(0, 16), false, ks);
