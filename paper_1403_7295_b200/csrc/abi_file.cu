@@ -237,8 +237,10 @@ struct ReplacedOutput {
     const unsigned long long v = e ? std::strtoull(e, nullptr, 10) : 1;
     if (v == 0) return;
     const long long min_size = v == 1 ? (64ll << 20) : static_cast<long long>(v);
-    fd = ::open(path, O_RDONLY | O_CLOEXEC);
+    // only a plain file is ever opened (a FIFO would block in open, a device may have side effects)
     struct stat st {};
+    if (::stat(path, &st) != 0 || !S_ISREG(st.st_mode) || st.st_size < min_size) return;
+    fd = ::open(path, O_RDONLY | O_CLOEXEC | O_NONBLOCK | O_NOCTTY);
     if (fd >= 0 && (::fstat(fd, &st) != 0 || !S_ISREG(st.st_mode) || st.st_nlink != 1 || st.st_size < min_size)) {
       ::close(fd);
       fd = -1;
