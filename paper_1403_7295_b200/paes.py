@@ -79,8 +79,18 @@ class _InBuf:
         if self.n == 0:
             self.keep, self.ptr = mv, None
         elif mv.readonly:
-            self.keep = bytes(mv)
-            self.ptr = C.cast(C.c_char_p(self.keep), C.c_void_p).value
+            # ctypes cannot borrow a read-only buffer (a read-only mmap, a
+            # memoryview of bytes); numpy can, without the single-threaded
+            # bytes(mv) copy that would dominate a multi-GiB call
+            try:
+                import numpy as np
+
+                arr = np.frombuffer(mv, dtype=np.uint8)
+                self.keep = (mv, arr)
+                self.ptr = int(arr.ctypes.data)
+            except ImportError:
+                self.keep = bytes(mv)
+                self.ptr = C.cast(C.c_char_p(self.keep), C.c_void_p).value
         else:
             arr = (C.c_uint8 * self.n).from_buffer(mv)
             self.keep = (mv, arr)

@@ -340,3 +340,29 @@ def test_stale_library_warns_instead_of_loading_silently(monkeypatch):
         L = _native.load()
     assert L is not None
     assert any("older than its sources" in str(x.message) for x in w)
+
+
+def test_input_buffers_are_borrowed_whatever_their_kind(paes, tmp_path):
+    """paes._InBuf: bytes, writable buffers and READ-ONLY buffers (memoryview
+    of bytes, read-only numpy array, read-only mmap of a file) all reach the
+    library by pointer -- a read-only buffer is not copied into a new bytes
+    object first (that single-threaded copy would dominate a multi-GiB call)."""
+    import mmap
+
+    import numpy as np
+
+    data = bytes(range(256)) * 5 + b"xyz"
+    want = data + bytes([16 - len(data) % 16]) * (16 - len(data) % 16)
+    ro = np.frombuffer(data, dtype=np.uint8)
+    assert not ro.flags.writeable
+    f = tmp_path / "in.bin"
+    f.write_bytes(data)
+    with open(f, "rb") as fh, mmap.mmap(fh.fileno(), 0, access=mmap.ACCESS_READ) as mm:
+        for buf in (data, bytearray(data), memoryview(data), ro, mm, memoryview(bytearray(data))[:]):
+            assert paes.pkcs7_pad(buf) == want, type(buf)
+            b = paes._InBuf(buf)
+            assert b.n == len(data)
+            if not isinstance(buf, bytes):
+                assert not isinstance(b.keep, bytes), type(buf)  # borrowed, not copied
+            del b
+    assert paes.pkcs7_pad(memoryview(b"")) == bytes([16]) * 16
