@@ -25,8 +25,10 @@ configs : (N = 1, rank 0) every other BASELINE.json config on the driver's
           clock -- configs 1, 2, 3 (six sizes), 5, device-resident and end to
           end, each with its parity verdict against tests/golden/digests.json
           (reference-computed); plus the pageable-memory e2e through
-          encrypt_bytes and the paper's own file -> file metric (run_job on
-          /dev/shm) next to the reference's run_job(threads).
+          encrypt_bytes, the C++ drop-in (paes::gpu::encrypt_chunk on a 4 GiB
+          std::vector, compiled here from scripts/shim_chunk_probe.cpp) and the
+          paper's own file -> file metric (run_job on /dev/shm) next to the
+          reference's run_job(threads).
 --impl reference : the reference's own CPU path (oracle/_ref, compiled from the
           reference sources) on all host cores, rank 0 only.
 """
