@@ -97,7 +97,6 @@ class Prealloc {
     active_ = true;
     th_ = std::thread([this] { run(); });
   }
-  bool active() const { return active_; }
 
   // Blocks until bytes [off, off + len) of the file are allocated; false when
   // the allocation failed (the caller reports the write failure).
