@@ -331,7 +331,16 @@ std::uint64_t file_shard(DevCtx& d, const Range& r, int in_fd, int out_fd, std::
                          std::uint64_t in_off, std::uint64_t out_off, const KeyWords& kw, const std::string& in_path,
                          const std::string& out_path, unsigned io_threads) {
   DeviceGuard g(d.id);
-  ensure_pipeline(d, true);
+  {
+    const auto t0 = std::chrono::steady_clock::now();
+    ensure_pipeline(d, false);
+    // pinned host slots sized to this job's piece, not to the device slot
+    ensure_host_ring(d, piece_size(r.in_len, d.chunk, static_cast<int>(d.st.size())));  // slots carry 16 spare bytes for the pad block
+    if (std::getenv("PAES_FILE_TRACE"))
+      std::fprintf(stderr, "[paes file] rings ready in %.3f s (host slots %llu MiB)\n",
+                   std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count(),
+                   static_cast<unsigned long long>(d.hbuf_bytes >> 20));
+  }
   // on an exception, drain the slots' streams before d.mu is released: a
   // queued H2D may still read a pinned slot the next job would refill
   QuiesceOnThrow quiesce{d};
@@ -454,7 +463,12 @@ extern "C" int paes_cuda_run_job(const char* input_path, const char* output_path
       r.pad = !dec && c.is_final;
       r.check_pad = dec && c.is_final;
       try {
+        const auto td = std::chrono::steady_clock::now();
         DevCtx& d = device(devs[i]);
+        if (std::getenv("PAES_FILE_TRACE"))
+          std::fprintf(stderr, "[paes file] device context %.3f s (job clock at %.3f s)\n",
+                       std::chrono::duration<double>(std::chrono::steady_clock::now() - td).count(),
+                       std::chrono::duration<double>(td - t0).count());
         std::lock_guard<std::mutex> lk(d.mu);
         const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
         const unsigned io = g_io_threads_per_shard

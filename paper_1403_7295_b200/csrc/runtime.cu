@@ -195,6 +195,7 @@ void ensure_pipeline(DevCtx& d, bool need_host) {
     }
     d.dbuf.clear();
     d.hbuf.clear();
+    d.hbuf_bytes = 0;
     d.sin_buf.clear();
     d.sout_buf.clear();
     d.obuf.clear();
@@ -229,21 +230,34 @@ void ensure_pipeline(DevCtx& d, bool need_host) {
     }
     d.chunk = chunk;
   }
-  if (need_host && static_cast<int>(d.hbuf.size()) != ns) {
+  if (need_host) ensure_host_ring(d, d.chunk);
+}
+
+// Pinning is the expensive part of building the rings (3 x 256 MiB of
+// cudaMallocHost cost ~0.3 s of a fresh process's first file job,
+// scripts/file_cold_probe.py), and file pieces are at most 64 MiB up to 16 GiB
+// of input (piece_size), so the host slots follow the job's piece.
+void ensure_host_ring(DevCtx& d, std::uint64_t bytes) {
+  const std::size_t ns = d.st.size();
+  std::uint64_t want = 16ull << 20;
+  while (want < bytes) want <<= 1;
+  want = std::min<std::uint64_t>(want, std::max<std::uint64_t>(d.chunk, bytes));
+  if (d.hbuf.size() == ns && d.hbuf_bytes >= want) return;
+  for (auto p : d.hbuf) cudaFreeHost(p);
+  d.hbuf.clear();
+  d.hbuf_bytes = 0;
+  try {
+    for (std::size_t i = 0; i < ns; ++i) {
+      std::uint8_t* p = nullptr;
+      PAES_CK(cudaMallocHost(&p, want + 16));
+      d.hbuf.push_back(p);
+    }
+  } catch (...) {
     for (auto p : d.hbuf) cudaFreeHost(p);
     d.hbuf.clear();
-    try {
-      for (int i = 0; i < ns; ++i) {
-        std::uint8_t* p = nullptr;
-        PAES_CK(cudaMallocHost(&p, d.chunk + 16));
-        d.hbuf.push_back(p);
-      }
-    } catch (...) {
-      for (auto p : d.hbuf) cudaFreeHost(p);
-      d.hbuf.clear();
-      throw;
-    }
+    throw;
   }
+  d.hbuf_bytes = want;
 }
 
 std::vector<int> device_list(int ngpus) {

@@ -114,7 +114,8 @@ struct DevCtx {
   std::mutex mu;  // serialises host-pointer pipelines / status words on this device
   std::vector<cudaStream_t> st;
   std::vector<std::uint8_t*> dbuf;  // chunk + 16 bytes each
-  std::vector<std::uint8_t*> hbuf;  // pinned staging for the file path
+  std::vector<std::uint8_t*> hbuf;  // pinned staging for the file path, hbuf_bytes + 16 each (ensure_host_ring)
+  std::uint64_t hbuf_bytes = 0;
   // staged ring for pageable host buffers: pinned input and output slots
   // (kStagedSlot bytes + 16 each) and one copy team per direction
   std::vector<std::uint8_t*> sin_buf, sout_buf;
@@ -158,6 +159,10 @@ class StatusSlot {
 };
 // Pipeline buffers (device ring, optional pinned host ring); d.mu held.
 void ensure_pipeline(DevCtx& d, bool need_host);
+// The file path's pinned host slots, sized to the job's piece instead of the
+// device slot: grow-only, `bytes` rounded up to a power of two between 16 MiB
+// and the configured chunk.  Call after ensure_pipeline(d, false); d.mu held.
+void ensure_host_ring(DevCtx& d, std::uint64_t bytes);
 // Pins the calling library-owned thread (and the threads it spawns) to the
 // CPUs of the device's NUMA node; a no-op where sysfs reports no node.
 void bind_thread_to_device_numa(int dev);
