@@ -21,7 +21,6 @@ sys.path.insert(0, ROOT)
 
 import numpy as np  # noqa: E402
 
-import oracle  # noqa: E402
 from paper_1403_7295_b200 import paes  # noqa: E402
 
 
@@ -45,15 +44,17 @@ def main():
     ap.add_argument("--env", default="PAES_FILE_ASYNC_RECLAIM",
                     help="the 0/1 switch to A/B (also PAES_FILE_PREALLOC: fallocate thread ahead of the mapped writers)")
     args = ap.parse_args()
-    O = oracle.Oracle()
-    key = O.sweep(3, 16)
+    key = bytes(range(16))
     src = os.path.join(args.dir, f"paes_ab_in_{os.getpid()}.bin")
     ct = os.path.join(args.dir, f"paes_ab_ct_{os.getpid()}.bin")
     pt = os.path.join(args.dir, f"paes_ab_pt_{os.getpid()}.bin")
-    buf = np.empty(args.size, dtype=np.uint8)
-    O.counter_fill_into(3, 0, args.size, buf.ctypes.data)
-    buf.tofile(src)
-    del buf
+    rng = np.random.default_rng(3)
+    with open(src, "wb") as f:
+        left = args.size
+        while left:
+            n = min(left, 256 << 20)
+            f.write(rng.integers(0, 256, n, dtype=np.uint8).tobytes())
+            left -= n
     res = {"size": args.size, "dir": args.dir, "reps": args.reps, "switch": args.env}
     try:
         paes.encrypt_file(src, ct, key, workers=1)  # warm: context, ring, page cache

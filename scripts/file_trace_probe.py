@@ -1,12 +1,23 @@
+"""PAES_FILE_TRACE timeline of run_job on /dev/shm (4 GiB + 7): the Prealloc thread's run time and the writers'
+total wait, with a replaced output reclaimed on a detached thread (1) or inside rename (0), and with no old
+output at all (last two reps).  Developer probe; prints to stdout/stderr.
+
+    python scripts/file_trace_probe.py
+"""
 import os, sys, time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
-import oracle
 from paper_1403_7295_b200 import paes
-O = oracle.Oracle(); key = O.sweep(3,16)
+key = bytes(range(16))
 n=(4<<30)+7
 src='/dev/shm/paes_tr_in.bin'; ct='/dev/shm/paes_tr_ct.bin'
-buf=np.empty(n,dtype=np.uint8); O.counter_fill_into(3,0,n,buf.ctypes.data); buf.tofile(src); del buf
+rng = np.random.default_rng(3)
+with open(src, 'wb') as f:
+    left = n
+    while left:
+        m = min(left, 256 << 20)
+        f.write(rng.integers(0, 256, m, dtype=np.uint8).tobytes())
+        left -= m
 paes.encrypt_file(src,ct,key,workers=1)
 os.environ['PAES_FILE_TRACE']='1'
 for rec in ('1','0'):
